@@ -1,0 +1,81 @@
+"""Loader and ctypes signatures of libpgb200.so (include/pulsegrid_b200.h).
+
+The library is built in-tree (paper_2512_00398_b200/libpgb200.so, by
+csrc/Makefile via __graft_entry__.build()).  There is no CPU fallback: if the
+library is missing, importing this module raises, and on a machine without an
+sm_100 GPU every context creation fails with DeviceError.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from pathlib import Path
+
+from . import abi
+from .errors import raise_for
+
+LIB_PATH = Path(__file__).resolve().parent / "libpgb200.so"
+
+if not LIB_PATH.exists():
+    raise ImportError(
+        f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(make -C paper_2512_00398_b200/csrc).  There is no CPU fallback.")
+
+lib = ctypes.CDLL(str(LIB_PATH), mode=os.RTLD_LOCAL)
+
+_c = ctypes
+_vp, _u32, _u64, _sz, _int = _c.c_void_p, _c.c_uint32, _c.c_uint64, _c.c_size_t, _c.c_int
+_P = _c.POINTER
+
+SIGNATURES = {
+    "pgb_abi_version": ([], _int),
+    "pgb_last_error": ([], _c.c_char_p),
+    "pgb_device_count": ([_P(_int)], _int),
+    "pgb_delay_samples": ([_c.c_double, _P(abi.HeaderC), _u32], _c.c_int64),
+    "pgb_adaptive_dm_step": ([_c.c_double, _P(abi.HeaderC)], _c.c_double),
+    "pgb_generate_dm_trials": ([_c.c_double, _c.c_double, _P(abi.HeaderC), _int, _c.c_double, _vp,
+                                _vp, _sz, _P(_sz)], _int),
+    "pgb_create": ([_int, _P(_vp)], _int),
+    "pgb_destroy": ([_vp], _int),
+    "pgb_set_plan": ([_vp, _vp, _vp, _u32, _u32], _int),
+    "pgb_set_trial_range": ([_vp, _u32, _u32], _int),
+    "pgb_run_dm_loop_u8": ([_vp, _vp, _int, _P(abi.ChunkSpecC), _P(abi.EngineConfigC), _P(_sz),
+                            _P(_sz)], _int),
+    "pgb_run_dm_loop_f32": ([_vp, _vp, _int, _P(abi.ChunkSpecC), _P(abi.EngineConfigC), _P(_sz),
+                             _P(_sz)], _int),
+    "pgb_fetch_candidates": ([_vp, _vp, _sz], _int),
+    "pgb_fetch_skipped": ([_vp, _vp, _sz], _int),
+    "pgb_device_candidates": ([_vp, _P(_vp), _P(_sz)], _int),
+    "pgb_dedisperse_u8": ([_vp, _vp, _u64, _u32, _u32, _vp, _u64], _int),
+    "pgb_dedisperse_f32": ([_vp, _vp, _u64, _u32, _u32, _vp, _u64], _int),
+    "pgb_link_grid": ([_vp, _vp, _int, _sz, _P(abi.LinkRadiiC), _P(_sz)], _int),
+    "pgb_fetch_clusters": ([_vp, _vp, _sz, _vp, _sz], _int),
+    "pgb_search_file_u8": ([_vp, _vp, _int, _u64, _vp, _sz, _P(abi.EngineConfigC),
+                            _P(abi.LinkRadiiC), _P(_sz), _P(_sz)], _int),
+    "pgb_fetch_file_candidates": ([_vp, _vp, _sz], _int),
+    "pgb_fetch_file_skipped": ([_vp, _vp, _sz, _P(_sz)], _int),
+    "pgb_launch_count": ([_vp, _P(_u64)], _int),
+    "pgb_last_dedisp_time": ([_vp, _P(_c.c_double), _P(_u64), _P(_u64)], _int),
+    "pgb_stream": ([_vp, _P(_vp)], _int),
+}
+
+for _name, (_args, _res) in SIGNATURES.items():
+    _f = getattr(lib, _name)
+    _f.argtypes = _args
+    _f.restype = _res
+
+
+def check(rc: int) -> None:
+    """Raise the pulsegrid exception named by a pgb_status."""
+    if rc:
+        raise_for(rc, lib.pgb_last_error().decode(errors="replace"))
+
+
+def device_count() -> int:
+    n = _int(0)
+    check(lib.pgb_device_count(_c.byref(n)))
+    return n.value
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)

@@ -1,0 +1,897 @@
+// C ABI of libpgb200 (include/pulsegrid_b200.h): contexts, plan upload, the
+// device run_dm_loop / link_grid / file search, and the host-side DM plan.
+//
+// Host orchestration per chunk (one CUDA stream per context, two host syncs):
+//   H2D (optional) -> transpose -> dedispersion -> baseline -> robust RMS ->
+//   boxcar ladder + runs -> [sync: counts] -> fragment sort + stitch ->
+//   candidate sort -> [sync: count, degenerate flags]
+// Results stay on the device until fetched (pgb_fetch_*).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <numeric>
+#include <stdexcept>
+
+#include "pgb_internal.h"
+
+namespace pgb {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+void raise(pgb_status code, const std::string& msg) { throw Error{code, msg}; }
+
+void check_cuda(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return;
+    const pgb_status code = (e == cudaErrorMemoryAllocation) ? PGB_ERR_OOM : PGB_ERR_CUDA;
+    raise(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+void DevBuf::reserve(size_t n, bool zero) {
+    if (n <= bytes && p) return;
+    release();
+    const size_t want = std::max<size_t>(n, 256);
+    PGB_CUDA(cudaMalloc(&p, want));
+    bytes = want;
+    if (zero) PGB_CUDA(cudaMemset(p, 0, want));
+}
+void DevBuf::release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+}
+void PinnedBuf::reserve(size_t n) {
+    if (n <= bytes && p) return;
+    release();
+    PGB_CUDA(cudaMallocHost(&p, std::max<size_t>(n, 256)));
+    bytes = std::max<size_t>(n, 256);
+}
+void PinnedBuf::release() {
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+}
+
+// ---- host DM plan, bit-identical to the reference build ------------------------
+// (the reference's -ffp-contract=fast turns fch1 + foff*c and dm_lo + i*step into
+// FMAs; this TU is compiled with -ffp-contract=off and spells them out.)
+
+constexpr double k_dispersion = 4.148808e3;  // dedisp.hpp:13
+
+double channel_freq(const pgb_header* h, uint32_t c) { return std::fma(h->foff, (double)c, h->fch1); }
+double max_freq(const pgb_header* h) { return h->foff >= 0 ? channel_freq(h, h->nchans - 1) : h->fch1; }
+double min_freq(const pgb_header* h) { return h->foff >= 0 ? h->fch1 : channel_freq(h, h->nchans - 1); }
+
+int64_t delay_samples(double dm, const pgb_header* h, uint32_t c) {  // src/dedisp.cpp:13-18
+    const double f_ref = max_freq(h);
+    const double f_c = channel_freq(h, c);
+    const double delay_s = k_dispersion * dm * (1.0 / (f_c * f_c) - 1.0 / (f_ref * f_ref));
+    return (int64_t)std::floor(delay_s / h->tsamp + 0.5);
+}
+
+double adaptive_step(double tol, const pgb_header* h) {  // src/dedisp.cpp:20-26
+    const double f_lo = min_freq(h), f_hi = max_freq(h);
+    const double band = 1.0 / (f_lo * f_lo) - 1.0 / (f_hi * f_hi);
+    if (band <= 0.0) return 0.0;
+    return (tol - 1.0) * h->tsamp / (k_dispersion * band);
+}
+
+// BufferPool::aligned_size (src/buffer_pool.cpp:22-24)
+static size_t pool_aligned(size_t n) {
+    size_t v = std::max<size_t>(n, 256);
+    size_t p = 1;
+    while (p < v) p <<= 1;
+    return p;
+}
+
+}  // namespace pgb
+
+using namespace pgb;
+
+struct pgb_context {
+    int device = 0;
+    cudaStream_t st = nullptr;
+    cudaStream_t copy_st = nullptr;
+    cudaEvent_t ev_dd0 = nullptr, ev_dd1 = nullptr;
+    std::vector<cudaEvent_t> seg_events;
+
+    // plan
+    uint32_t ntrials = 0, nchans = 0;
+    std::vector<double> dms;
+    std::vector<int64_t> delays;  // host copy [T][C]
+    std::vector<int64_t> maxd;
+    DevBuf d_delays_ct, d_dms;
+    uint32_t tr_begin = 0, tr_end = 0;
+
+    // per-chunk geometry cache (keyed on the active trial list)
+    std::vector<uint32_t> active;
+    std::vector<uint32_t> blk_spread;  // per 32-row block
+    bool geom_valid = false;
+
+    // device work buffers
+    DevBuf in_raw, rows, series, base, frms, status, d_active, d_row_len, d_blk_len, d_scale;
+    DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
+    DevBuf payload;
+    DevBuf file_cands, file_sorted;
+    DevBuf cl_scratch, clusters, members;
+    PinnedBuf h_counters;
+
+    uint64_t cand_cap = 1 << 16, frag_cap = 1 << 16;
+
+    // results
+    uint64_t n_cands = 0;
+    std::vector<uint64_t> skipped;
+    uint64_t n_clusters = 0, n_members = 0;
+    uint64_t file_ncands = 0;
+    std::vector<uint64_t> file_skipped;  // (chunk, trial) pairs
+    bool last_from_file = false;
+
+    // instrumentation
+    uint64_t launches = 0;
+    double dedisp_ms = 0.0;
+    uint64_t dedisp_launches = 0;
+    uint64_t channel_adds = 0;
+    // last chunk's row geometry for stage fetches
+    uint64_t last_out_pitch = 0;
+    uint32_t last_nrows = 0;
+    bool last_had_baseline = false;
+    bool last_u8 = true;
+};
+
+namespace {
+
+template <typename F>
+pgb_status guarded(F&& f) {
+    try {
+        f();
+        return PGB_OK;
+    } catch (const Error& e) {
+        g_last_error = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_last_error = "host allocation failed";
+        return PGB_ERR_OOM;
+    } catch (const std::exception& e) {
+        g_last_error = e.what();
+        return PGB_ERR_ARGUMENT;
+    }
+}
+
+void need(bool cond, pgb_status code, const char* msg) {
+    if (!cond) raise(code, msg);
+}
+
+struct ChunkInput {
+    const void* data;   // device pointer, time-major
+    bool u8;
+};
+
+// Validation and in-flight arithmetic of run_dm_loop (src/engine.cpp:60-97).
+void validate_cfg(pgb_context* ctx, const pgb_chunk_spec* spec, const pgb_engine_config* cfg) {
+    need(spec && cfg, PGB_ERR_ARGUMENT, "null spec/config");
+    if (cfg->n_workers < 1) raise(PGB_ERR_CONFIG, "n_workers must be >= 1");
+    if (cfg->boxcar_max < 1 || (cfg->boxcar_max & (cfg->boxcar_max - 1)) != 0)
+        raise(PGB_ERR_CONFIG, "boxcar_max must be a power of two");
+    if (cfg->boxcar_max > 8192)
+        raise(PGB_ERR_CONFIG, "boxcar_max > 8192 is not supported by the device path");
+    if (ctx->ntrials == 0) return;
+    if (cfg->max_in_flight == 0) {  // in_flight_limit, src/engine.cpp:75-83
+        const int64_t min_delay = ctx->maxd[0];
+        const uint64_t length = spec->length;
+        const uint64_t longest = length > (uint64_t)min_delay ? length - (uint64_t)min_delay : 1;
+        const size_t series_bytes = pool_aligned(longest * sizeof(float));
+        const uint64_t n_blocks = (longest + 63) / 64;
+        const size_t sums_bytes = pool_aligned((longest + n_blocks) * sizeof(double));
+        const size_t buffers = cfg->baseline_window > 0 ? 2 : 1;
+        const size_t ws = buffers * series_bytes + sums_bytes;
+        if (cfg->memory_budget / ws == 0)
+            raise(PGB_ERR_CONFIG, "memory budget of " + std::to_string(cfg->memory_budget) +
+                                      " bytes is below one trial's working set (" +
+                                      std::to_string(ws) + ")");
+    }
+}
+
+uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+// Runs the whole chain for one chunk whose samples are already on the device.
+void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spec,
+               const pgb_engine_config* cfg) {
+    cudaStream_t st = ctx->st;
+    const uint64_t L = spec->length;
+    const uint32_t C = ctx->nchans;
+    ctx->n_cands = 0;
+    ctx->skipped.clear();
+    ctx->last_nrows = 0;
+    if (ctx->ntrials == 0 || L == 0) return;
+
+    // active rows: trials whose span fits the chunk (src/engine.cpp:112-118)
+    std::vector<uint32_t> active;
+    active.reserve(ctx->tr_end - ctx->tr_begin);
+    for (uint32_t t = ctx->tr_begin; t < ctx->tr_end; ++t) {
+        if ((uint64_t)ctx->maxd[t] >= L) ctx->skipped.push_back(t);
+        else active.push_back(t);
+    }
+    const uint32_t nrows = (uint32_t)active.size();
+    if (nrows == 0) return;
+    if (ctx->nchans > 0 && nrows > (1u << 20)) raise(PGB_ERR_CONFIG, "more than 2^20 trials");
+
+    std::vector<uint32_t> row_len(nrows);
+    uint64_t max_n = 0, maxd_active = 0;
+    for (uint32_t r = 0; r < nrows; ++r) {
+        row_len[r] = (uint32_t)(L - (uint64_t)ctx->maxd[active[r]]);
+        max_n = std::max<uint64_t>(max_n, row_len[r]);
+        maxd_active = std::max<uint64_t>(maxd_active, (uint64_t)ctx->maxd[active[r]]);
+    }
+    // per 32-row block: longest series and channel window spread (cached per active set)
+    const int tpw = 2, tb = DD_WARPS * tpw;
+    const uint32_t nblocks = (nrows + tb - 1) / tb;
+    if (!ctx->geom_valid || ctx->active != active) {
+        ctx->blk_spread.assign(nblocks, 0);
+        for (uint32_t b = 0; b < nblocks; ++b) {
+            const uint32_t r0 = b * tb, r1 = std::min(nrows, r0 + tb);
+            uint32_t sp = 0;
+            for (uint32_t c = 0; c < C; ++c) {
+                int64_t lo = INT64_MAX, hi = INT64_MIN;
+                for (uint32_t r = r0; r < r1; ++r) {
+                    const int64_t d = ctx->delays[(size_t)active[r] * C + c];
+                    lo = std::min(lo, d);
+                    hi = std::max(hi, d);
+                }
+                sp = std::max<uint32_t>(sp, (uint32_t)(hi - lo));
+            }
+            ctx->blk_spread[b] = sp;
+        }
+        ctx->active = active;
+        ctx->geom_valid = true;
+        ctx->d_active.reserve(nrows * sizeof(uint32_t));
+        PGB_CUDA(cudaMemcpyAsync(ctx->d_active.p, active.data(), nrows * sizeof(uint32_t),
+                                 cudaMemcpyHostToDevice, st));
+    }
+    std::vector<uint32_t> blk_len(nblocks, 0);
+    for (uint32_t r = 0; r < nrows; ++r) blk_len[r / tb] = std::max(blk_len[r / tb], row_len[r]);
+    const uint32_t spread = *std::max_element(ctx->blk_spread.begin(), ctx->blk_spread.end());
+
+    const bool u8 = in.u8;
+    const uint32_t align_el = u8 ? 16 : 4;
+    const uint32_t wmax = (uint32_t)round_up(spread + DD_NT + 2 * align_el + 16, 16);
+    int g = 8;
+    while (g > 1 && dedisp_smem_bytes(u8, g, wmax) > DD_SMEM_BUDGET) g >>= 1;
+    if (dedisp_smem_bytes(u8, g, wmax) > DD_SMEM_BUDGET || (u8 && (uint64_t)g * wmax / 16 > 4ull * DD_THREADS))
+        raise(PGB_ERR_CONFIG, "per-block channel delay spread of " + std::to_string(spread) +
+                                  " samples exceeds the dedispersion staging capacity");
+    const uint32_t ntiles = (uint32_t)((max_n + DD_NT - 1) / DD_NT);
+    const uint64_t out_pitch = (uint64_t)ntiles * DD_NT;
+    const uint64_t rows_pitch = round_up((uint64_t)ntiles * DD_NT + maxd_active + wmax + 64, 64);
+    const size_t esz = u8 ? 1 : 4;
+
+    ctx->rows.reserve((size_t)C * rows_pitch * esz, true);
+    ctx->series.reserve((size_t)nrows * out_pitch * 4);
+    const bool baseline = cfg->baseline_window > 0;
+    if (baseline) ctx->base.reserve((size_t)nrows * out_pitch * 4);
+    ctx->frms.reserve(nrows * sizeof(float));
+    ctx->status.reserve(nrows);
+    ctx->d_row_len.reserve(nrows * sizeof(uint32_t));
+    ctx->d_blk_len.reserve(nblocks * sizeof(uint32_t));
+    PGB_CUDA(cudaMemcpyAsync(ctx->d_row_len.p, row_len.data(), nrows * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, st));
+    PGB_CUDA(cudaMemcpyAsync(ctx->d_blk_len.p, blk_len.data(), nblocks * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, st));
+    // ladder scales 1/sqrt(w) (src/engine.cpp:207), computed on the host like the reference
+    {
+        double sc[32];
+        for (int l = 0; l < 32; ++l) sc[l] = 1.0 / std::sqrt((double)(1ull << l));
+        ctx->d_scale.reserve(sizeof sc);
+        PGB_CUDA(cudaMemcpyAsync(ctx->d_scale.p, sc, sizeof sc, cudaMemcpyHostToDevice, st));
+    }
+
+    // 1. transpose to channel-major rows
+    if (u8)
+        launch_transpose_u8(static_cast<const uint8_t*>(in.data), L, C, ctx->rows.as<uint8_t>(),
+                            rows_pitch, st);
+    else
+        launch_transpose_f32(static_cast<const float*>(in.data), L, C, ctx->rows.as<float>(),
+                             rows_pitch, st);
+    // 2. dedispersion
+    DedispLaunch dl{};
+    dl.delays_ct = ctx->d_delays_ct.as<int32_t>();
+    dl.ntrials_plan = ctx->ntrials;
+    dl.nchans = C;
+    dl.active = ctx->d_active.as<uint32_t>();
+    dl.nrows = nrows;
+    dl.row_len = ctx->d_row_len.as<uint32_t>();
+    dl.blk_len = ctx->d_blk_len.as<uint32_t>();
+    dl.rows_pitch = rows_pitch;
+    dl.out_pitch = out_pitch;
+    dl.tpw = tpw;
+    dl.g = g;
+    dl.wmax = wmax;
+    dl.ntiles = ntiles;
+    PGB_CUDA(cudaEventRecord(ctx->ev_dd0, st));
+    if (u8) launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+    else launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
+    PGB_CUDA(cudaEventRecord(ctx->ev_dd1, st));
+    ctx->dedisp_launches += 1;
+    ctx->launches += 2;
+    uint64_t adds = 0;
+    for (uint32_t r = 0; r < nrows; ++r) adds += (uint64_t)row_len[r] * C;
+    ctx->channel_adds += adds;
+
+    // 3. baseline, 4. robust RMS
+    const void* work = ctx->series.p;
+    int kind = u8 ? 1 : 0;
+    if (baseline) {
+        const uint64_t w = cfg->baseline_window % 2 == 0 ? cfg->baseline_window + 1 : cfg->baseline_window;
+        if (u8)
+            launch_baseline_int(ctx->series.as<int32_t>(), ctx->base.as<float>(),
+                                ctx->d_row_len.as<uint32_t>(), nrows, out_pitch, w, st);
+        else
+            launch_baseline_f32(ctx->series.as<float>(), ctx->base.as<float>(),
+                                ctx->d_row_len.as<uint32_t>(), nrows, out_pitch, w, st);
+        work = ctx->base.p;
+        kind = 0;
+    }
+    launch_rms(work, kind, ctx->d_row_len.as<uint32_t>(), nrows, out_pitch, ctx->frms.as<float>(),
+               ctx->status.as<uint8_t>(), st);
+    ctx->launches += 5;
+
+    // 5. boxcar ladder + runs (re-run with larger buffers on overflow)
+    ChainParams cp{};
+    cp.start_sample = spec->start_sample;
+    cp.valid_begin = spec->valid_begin;
+    cp.valid_end = spec->valid_end;
+    cp.drop_left = spec->start_sample > 0;
+    cp.drop_right = spec->overlap > 0;
+    cp.tsamp = cfg->tsamp;
+    cp.threshold = (double)cfg->detect_thresh;
+    cp.boxcar_max = cfg->boxcar_max;
+    ctx->counters.reserve(4 * sizeof(unsigned long long));
+    ctx->h_counters.reserve(4 * sizeof(unsigned long long));
+    auto* dcnt = ctx->counters.as<unsigned long long>();
+    auto* hcnt = ctx->h_counters.as<unsigned long long>();
+    for (int attempt = 0;; ++attempt) {
+        ctx->cands_raw.reserve(ctx->cand_cap * sizeof(pgb_candidate));
+        ctx->frags.reserve(ctx->frag_cap * sizeof(Fragment));
+        PGB_CUDA(cudaMemsetAsync(dcnt, 0, 2 * sizeof(unsigned long long), st));
+        launch_boxcar_peaks(work, kind, ctx->d_row_len.as<uint32_t>(), ctx->frms.as<float>(),
+                            ctx->status.as<uint8_t>(), nrows, out_pitch, max_n, cp,
+                            ctx->d_active.as<uint32_t>(), ctx->d_dms.as<double>(),
+                            ctx->d_scale.as<double>(), ctx->cands_raw.as<pgb_candidate>(), dcnt,
+                            ctx->cand_cap, ctx->frags.as<Fragment>(), dcnt + 1, ctx->frag_cap, st);
+        PGB_CUDA(cudaMemcpyAsync(hcnt, dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+        PGB_CUDA(cudaStreamSynchronize(st));
+        const uint64_t nc = hcnt[0], nf = hcnt[1];
+        ctx->launches += 1;
+        if (nc > ctx->cand_cap || nf > ctx->frag_cap) {
+            ctx->cand_cap = std::max<uint64_t>(ctx->cand_cap, round_up(nc * 2, 1024));
+            ctx->frag_cap = std::max<uint64_t>(ctx->frag_cap, round_up(nf * 2, 1024));
+            continue;
+        }
+        if (nf) {
+            ctx->frags_sorted.reserve(nf * sizeof(Fragment));
+            const size_t tmp = sort_fragments_temp_bytes(nf);
+            ctx->sort_tmp.reserve(tmp);
+            ctx->sort_keys.reserve(2 * nf * sizeof(uint64_t));
+            ctx->sort_idx.reserve(2 * nf * sizeof(uint32_t));
+            sort_fragments(ctx->frags.as<Fragment>(), ctx->frags_sorted.as<Fragment>(), nf,
+                           ctx->sort_tmp.p, tmp, ctx->sort_keys.as<uint64_t>(),
+                           ctx->sort_keys.as<uint64_t>() + nf, ctx->sort_idx.as<uint32_t>(),
+                           ctx->sort_idx.as<uint32_t>() + nf, st);
+            launch_stitch(ctx->frags_sorted.as<Fragment>(), nf, ctx->d_row_len.as<uint32_t>(), cp,
+                          ctx->d_active.as<uint32_t>(), ctx->d_dms.as<double>(),
+                          ctx->cands_raw.as<pgb_candidate>(), dcnt, ctx->cand_cap, st);
+            PGB_CUDA(cudaMemcpyAsync(hcnt, dcnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
+            PGB_CUDA(cudaStreamSynchronize(st));
+            ctx->launches += 4;
+            if (hcnt[0] > ctx->cand_cap) {
+                ctx->cand_cap = round_up(hcnt[0] * 2, 1024);
+                continue;
+            }
+        }
+        ctx->n_cands = hcnt[0];
+        break;
+    }
+    // 6. candidate order
+    const uint64_t nc = ctx->n_cands;
+    ctx->cands_sorted.reserve(std::max<uint64_t>(nc, 1) * sizeof(pgb_candidate));
+    if (nc) {
+        const size_t tmp = sort_candidates_temp_bytes(nc);
+        ctx->sort_tmp.reserve(tmp);
+        ctx->sort_keys.reserve(2 * nc * sizeof(uint64_t));
+        ctx->sort_idx.reserve(2 * nc * sizeof(uint32_t));
+        sort_candidates(ctx->cands_raw.as<pgb_candidate>(), ctx->cands_sorted.as<pgb_candidate>(),
+                        nc, ctx->sort_tmp.p, tmp, ctx->sort_keys.as<uint64_t>(),
+                        ctx->sort_keys.as<uint64_t>() + nc, ctx->sort_idx.as<uint32_t>(),
+                        ctx->sort_idx.as<uint32_t>() + nc, st);
+        ctx->launches += 3;
+    }
+    // 7. degenerate trials (src/engine.cpp:189-194) join the uncoverable ones
+    std::vector<uint8_t> stat(nrows);
+    PGB_CUDA(cudaMemcpyAsync(stat.data(), ctx->status.p, nrows, cudaMemcpyDeviceToHost, st));
+    PGB_CUDA(cudaStreamSynchronize(st));
+    for (uint32_t r = 0; r < nrows; ++r)
+        if (stat[r]) ctx->skipped.push_back(active[r]);
+    std::sort(ctx->skipped.begin(), ctx->skipped.end());
+    float ms = 0.f;
+    PGB_CUDA(cudaEventElapsedTime(&ms, ctx->ev_dd0, ctx->ev_dd1));
+    ctx->dedisp_ms += ms;
+    ctx->last_out_pitch = out_pitch;
+    ctx->last_nrows = nrows;
+    ctx->last_had_baseline = baseline;
+    ctx->last_u8 = u8;
+}
+
+void reset_timing(pgb_context* ctx) {
+    ctx->dedisp_ms = 0.0;
+    ctx->dedisp_launches = 0;
+    ctx->channel_adds = 0;
+}
+
+}  // namespace
+
+extern "C" {
+
+int pgb_abi_version(void) { return PGB_ABI_VERSION; }
+
+const char* pgb_last_error(void) { return g_last_error.c_str(); }
+
+pgb_status pgb_device_count(int* count) {
+    return guarded([&] {
+        need(count != nullptr, PGB_ERR_ARGUMENT, "null count");
+        int n = 0;
+        const cudaError_t e = cudaGetDeviceCount(&n);
+        if (e != cudaSuccess) {
+            cudaGetLastError();
+            n = 0;
+        }
+        *count = n;
+    });
+}
+
+int64_t pgb_delay_samples(double dm, const pgb_header* header, uint32_t channel) {
+    return delay_samples(dm, header, channel);
+}
+
+double pgb_adaptive_dm_step(double tol, const pgb_header* header) { return adaptive_step(tol, header); }
+
+pgb_status pgb_generate_dm_trials(double dm_lo, double dm_hi, const pgb_header* h, pgb_spacing spacing,
+                                  double value, double* dms, int64_t* delays, size_t capacity,
+                                  size_t* ntrials) {
+    return guarded([&] {  // src/dedisp.cpp:28-70
+        need(h && ntrials, PGB_ERR_ARGUMENT, "null header/ntrials");
+        if (dm_lo < 0.0 || dm_hi < dm_lo)
+            raise(PGB_ERR_INVALID_RANGE, "invalid DM range [" + std::to_string(dm_lo) + ", " +
+                                             std::to_string(dm_hi) + "]");
+        double step;
+        if (spacing == PGB_SPACING_LINEAR) {
+            if (value <= 0.0) raise(PGB_ERR_INVALID_RANGE, "linear DM step must be positive");
+            step = value;
+        } else {
+            if (value <= 1.0) raise(PGB_ERR_INVALID_RANGE, "adaptive tolerance must exceed 1");
+            step = adaptive_step(value, h);
+        }
+        std::vector<double> out;
+        if (step <= 0.0 || dm_hi == dm_lo) {
+            out.push_back(dm_lo);
+            if (dm_hi != dm_lo) out.push_back(dm_hi);
+        } else {
+            const double eps = step * 1e-9;
+            for (size_t i = 0;; ++i) {
+                const double dm = std::fma((double)i, step, dm_lo);
+                if (dm >= dm_hi - eps) {
+                    out.push_back(dm_hi);
+                    break;
+                }
+                out.push_back(dm);
+            }
+        }
+        *ntrials = out.size();
+        if (!dms) return;
+        need(capacity >= out.size(), PGB_ERR_ARGUMENT, "capacity too small");
+        std::copy(out.begin(), out.end(), dms);
+        if (delays)
+            for (size_t t = 0; t < out.size(); ++t)
+                for (uint32_t c = 0; c < h->nchans; ++c)
+                    delays[t * h->nchans + c] = delay_samples(out[t], h, c);
+    });
+}
+
+pgb_status pgb_create(int device, pgb_context** out) {
+    return guarded([&] {
+        need(out != nullptr, PGB_ERR_ARGUMENT, "null ctx");
+        int n = 0;
+        if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0) {
+            cudaGetLastError();
+            raise(PGB_ERR_NO_DEVICE, "no CUDA device visible (libpgb200 has no CPU fallback)");
+        }
+        need(device >= 0 && device < n, PGB_ERR_NO_DEVICE, "device ordinal out of range");
+        cudaDeviceProp prop{};
+        PGB_CUDA(cudaGetDeviceProperties(&prop, device));
+        if (prop.major != 10 || prop.minor != 0)
+            raise(PGB_ERR_NO_DEVICE, std::string("libpgb200 is built for sm_100a; device is ") +
+                                         prop.name);
+        auto* ctx = new pgb_context();
+        ctx->device = device;
+        PGB_CUDA(cudaSetDevice(device));
+        PGB_CUDA(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
+        PGB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
+        PGB_CUDA(cudaEventCreate(&ctx->ev_dd0));
+        PGB_CUDA(cudaEventCreate(&ctx->ev_dd1));
+        *out = ctx;
+    });
+}
+
+pgb_status pgb_destroy(pgb_context* ctx) {
+    return guarded([&] {
+        if (!ctx) return;
+        cudaSetDevice(ctx->device);
+        cudaStreamSynchronize(ctx->st);
+        cudaStreamSynchronize(ctx->copy_st);
+        for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,
+                          &ctx->base, &ctx->frms, &ctx->status, &ctx->d_active, &ctx->d_row_len,
+                          &ctx->d_blk_len, &ctx->d_scale, &ctx->cands_raw, &ctx->cands_sorted,
+                          &ctx->frags, &ctx->frags_sorted, &ctx->counters, &ctx->sort_keys,
+                          &ctx->sort_idx, &ctx->sort_tmp, &ctx->payload, &ctx->file_cands,
+                          &ctx->file_sorted, &ctx->cl_scratch, &ctx->clusters, &ctx->members})
+            b->release();
+        ctx->h_counters.release();
+        for (auto e : ctx->seg_events) cudaEventDestroy(e);
+        cudaEventDestroy(ctx->ev_dd0);
+        cudaEventDestroy(ctx->ev_dd1);
+        cudaStreamDestroy(ctx->st);
+        cudaStreamDestroy(ctx->copy_st);
+        delete ctx;
+    });
+}
+
+pgb_status pgb_set_plan(pgb_context* ctx, const double* dms, const int64_t* delays, uint32_t ntrials,
+                        uint32_t nchans) {
+    return guarded([&] {
+        need(ctx && (ntrials == 0 || (dms && delays)), PGB_ERR_ARGUMENT, "null plan");
+        need(nchans > 0 || ntrials == 0, PGB_ERR_ARGUMENT, "nchans must be positive");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        ctx->ntrials = ntrials;
+        ctx->nchans = nchans;
+        ctx->dms.assign(dms, dms + ntrials);
+        ctx->delays.assign(delays, delays + (size_t)ntrials * nchans);
+        ctx->maxd.assign(ntrials, 0);
+        std::vector<int32_t> ct((size_t)ntrials * nchans);
+        for (uint32_t t = 0; t < ntrials; ++t) {
+            int64_t m = INT64_MIN;
+            for (uint32_t c = 0; c < nchans; ++c) {
+                const int64_t d = delays[(size_t)t * nchans + c];
+                if (d < 0 || d > INT32_MAX) raise(PGB_ERR_INVALID_PLAN, "delay out of range");
+                m = std::max(m, d);
+                ct[(size_t)c * ntrials + t] = (int32_t)d;
+            }
+            ctx->maxd[t] = m;
+        }
+        ctx->tr_begin = 0;
+        ctx->tr_end = ntrials;
+        ctx->geom_valid = false;
+        if (ntrials) {
+            ctx->d_delays_ct.reserve(ct.size() * sizeof(int32_t));
+            ctx->d_dms.reserve(ntrials * sizeof(double));
+            PGB_CUDA(cudaMemcpyAsync(ctx->d_delays_ct.p, ct.data(), ct.size() * sizeof(int32_t),
+                                     cudaMemcpyHostToDevice, ctx->st));
+            PGB_CUDA(cudaMemcpyAsync(ctx->d_dms.p, dms, ntrials * sizeof(double),
+                                     cudaMemcpyHostToDevice, ctx->st));
+            PGB_CUDA(cudaStreamSynchronize(ctx->st));
+        }
+    });
+}
+
+pgb_status pgb_set_trial_range(pgb_context* ctx, uint32_t begin, uint32_t end) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        need(begin <= end && end <= ctx->ntrials, PGB_ERR_ARGUMENT, "trial range out of plan");
+        ctx->tr_begin = begin;
+        ctx->tr_end = end;
+        ctx->geom_valid = false;
+    });
+}
+
+static pgb_status run_dm_loop_impl(pgb_context* ctx, const void* data, bool u8, int on_device,
+                                   const pgb_chunk_spec* spec, const pgb_engine_config* cfg,
+                                   size_t* n_candidates, size_t* n_skipped) {
+    return guarded([&] {
+        need(ctx && data, PGB_ERR_ARGUMENT, "null ctx/data");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        validate_cfg(ctx, spec, cfg);
+        reset_timing(ctx);
+        ctx->last_from_file = false;
+        const void* dptr = data;
+        const size_t bytes = (size_t)spec->length * ctx->nchans * (u8 ? 1 : 4);
+        if (!on_device && ctx->ntrials) {
+            ctx->in_raw.reserve(bytes);
+            PGB_CUDA(cudaMemcpyAsync(ctx->in_raw.p, data, bytes, cudaMemcpyHostToDevice, ctx->st));
+            dptr = ctx->in_raw.p;
+        }
+        run_chunk(ctx, ChunkInput{dptr, u8}, spec, cfg);
+        if (n_candidates) *n_candidates = ctx->n_cands;
+        if (n_skipped) *n_skipped = ctx->skipped.size();
+    });
+}
+
+pgb_status pgb_run_dm_loop_u8(pgb_context* ctx, const uint8_t* data, int on_device,
+                              const pgb_chunk_spec* spec, const pgb_engine_config* cfg,
+                              size_t* n_candidates, size_t* n_skipped) {
+    return run_dm_loop_impl(ctx, data, true, on_device, spec, cfg, n_candidates, n_skipped);
+}
+
+pgb_status pgb_run_dm_loop_f32(pgb_context* ctx, const float* data, int on_device,
+                               const pgb_chunk_spec* spec, const pgb_engine_config* cfg,
+                               size_t* n_candidates, size_t* n_skipped) {
+    return run_dm_loop_impl(ctx, data, false, on_device, spec, cfg, n_candidates, n_skipped);
+}
+
+pgb_status pgb_fetch_candidates(pgb_context* ctx, pgb_candidate* out, size_t capacity) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        const uint64_t n = ctx->last_from_file ? ctx->file_ncands : ctx->n_cands;
+        need(capacity >= n && (n == 0 || out), PGB_ERR_ARGUMENT, "capacity too small");
+        if (!n) return;
+        const DevBuf& src = ctx->last_from_file ? ctx->file_sorted : ctx->cands_sorted;
+        PGB_CUDA(cudaMemcpyAsync(out, src.p, n * sizeof(pgb_candidate), cudaMemcpyDeviceToHost, ctx->st));
+        PGB_CUDA(cudaStreamSynchronize(ctx->st));
+    });
+}
+
+pgb_status pgb_fetch_skipped(pgb_context* ctx, uint64_t* out, size_t capacity) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        need(capacity >= ctx->skipped.size(), PGB_ERR_ARGUMENT, "capacity too small");
+        std::copy(ctx->skipped.begin(), ctx->skipped.end(), out);
+    });
+}
+
+pgb_status pgb_device_candidates(pgb_context* ctx, const pgb_candidate** dev_ptr, size_t* n) {
+    return guarded([&] {
+        need(ctx && dev_ptr && n, PGB_ERR_ARGUMENT, "null argument");
+        if (ctx->last_from_file) {
+            *dev_ptr = ctx->file_sorted.as<pgb_candidate>();
+            *n = ctx->file_ncands;
+        } else {
+            *dev_ptr = ctx->cands_sorted.as<pgb_candidate>();
+            *n = ctx->n_cands;
+        }
+    });
+}
+
+static pgb_status dedisperse_impl(pgb_context* ctx, const void* data, bool u8, uint64_t length,
+                                  uint32_t tb, uint32_t te, float* out, uint64_t out_stride) {
+    return guarded([&] {
+        need(ctx && data && out, PGB_ERR_ARGUMENT, "null argument");
+        need(tb <= te && te <= ctx->ntrials, PGB_ERR_ARGUMENT, "trial range out of plan");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        for (uint32_t t = tb; t < te; ++t)  // src/dedisp.cpp:137-142
+            if ((uint64_t)ctx->maxd[t] >= length)
+                raise(PGB_ERR_CHUNK_TOO_SHORT,
+                      "trial " + std::to_string(t) + ": chunk of " + std::to_string(length) +
+                          " samples cannot cover delay span " + std::to_string(ctx->maxd[t]));
+        if (tb == te) return;
+        const uint32_t save_b = ctx->tr_begin, save_e = ctx->tr_end;
+        ctx->tr_begin = tb;
+        ctx->tr_end = te;
+        ctx->geom_valid = false;
+        const size_t bytes = (size_t)length * ctx->nchans * (u8 ? 1 : 4);
+        ctx->in_raw.reserve(bytes);
+        PGB_CUDA(cudaMemcpyAsync(ctx->in_raw.p, data, bytes, cudaMemcpyHostToDevice, ctx->st));
+        // dedispersion only: reuse run_chunk's geometry by running the chain with
+        // a zero-width config is wasteful; replicate the first two stages instead.
+        pgb_chunk_spec spec{0, 0, length, 0, 0, length};
+        pgb_engine_config cfg{1, 1e30f, 0.0, 1, 0, 0, 1};
+        try {
+            run_chunk(ctx, ChunkInput{ctx->in_raw.p, u8}, &spec, &cfg);
+        } catch (...) {
+            ctx->tr_begin = save_b;
+            ctx->tr_end = save_e;
+            ctx->geom_valid = false;
+            throw;
+        }
+        ctx->tr_begin = save_b;
+        ctx->tr_end = save_e;
+        ctx->geom_valid = false;
+        const uint32_t nrows = te - tb;
+        const uint64_t pitch = ctx->last_out_pitch;
+        std::vector<float> host((size_t)nrows * pitch);
+        if (u8) {
+            std::vector<int32_t> tmp((size_t)nrows * pitch);
+            PGB_CUDA(cudaMemcpy(tmp.data(), ctx->series.p, tmp.size() * 4, cudaMemcpyDeviceToHost));
+            for (size_t i = 0; i < tmp.size(); ++i) host[i] = (float)tmp[i];
+        } else {
+            PGB_CUDA(cudaMemcpy(host.data(), ctx->series.p, host.size() * 4, cudaMemcpyDeviceToHost));
+        }
+        for (uint32_t r = 0; r < nrows; ++r) {
+            const uint64_t n = length - (uint64_t)ctx->maxd[tb + r];
+            std::memcpy(out + (size_t)r * out_stride, host.data() + (size_t)r * pitch, n * sizeof(float));
+        }
+    });
+}
+
+pgb_status pgb_dedisperse_u8(pgb_context* ctx, const uint8_t* data, uint64_t length,
+                             uint32_t trial_begin, uint32_t trial_end, float* out,
+                             uint64_t out_stride) {
+    return dedisperse_impl(ctx, data, true, length, trial_begin, trial_end, out, out_stride);
+}
+
+pgb_status pgb_dedisperse_f32(pgb_context* ctx, const float* data, uint64_t length,
+                              uint32_t trial_begin, uint32_t trial_end, float* out,
+                              uint64_t out_stride) {
+    return dedisperse_impl(ctx, data, false, length, trial_begin, trial_end, out, out_stride);
+}
+
+pgb_status pgb_link_grid(pgb_context* ctx, const pgb_candidate* cands, int on_device, size_t n,
+                         const pgb_link_radii* radii, size_t* n_clusters) {
+    return guarded([&] {
+        need(ctx && radii && (n == 0 || cands), PGB_ERR_ARGUMENT, "null argument");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        const pgb_candidate* dptr = cands;
+        if (!on_device && n) {
+            ctx->file_cands.reserve(n * sizeof(pgb_candidate));
+            PGB_CUDA(cudaMemcpyAsync(ctx->file_cands.p, cands, n * sizeof(pgb_candidate),
+                                     cudaMemcpyHostToDevice, ctx->st));
+            dptr = ctx->file_cands.as<pgb_candidate>();
+        }
+        uint64_t ncl = 0;
+        cluster_candidates(dptr, n, *radii, ctx->cl_scratch, ctx->clusters, ctx->members, &ncl,
+                           ctx->st, &ctx->launches);
+        PGB_CUDA(cudaStreamSynchronize(ctx->st));
+        ctx->n_clusters = ncl;
+        ctx->n_members = n;
+        if (n_clusters) *n_clusters = ncl;
+    });
+}
+
+pgb_status pgb_fetch_clusters(pgb_context* ctx, pgb_cluster* out, size_t capacity,
+                              uint64_t* member_ids, size_t member_capacity) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        need(capacity >= ctx->n_clusters, PGB_ERR_ARGUMENT, "cluster capacity too small");
+        if (ctx->n_clusters && out)
+            PGB_CUDA(cudaMemcpyAsync(out, ctx->clusters.p, ctx->n_clusters * sizeof(pgb_cluster),
+                                     cudaMemcpyDeviceToHost, ctx->st));
+        if (member_ids && ctx->n_members) {
+            need(member_capacity >= ctx->n_members, PGB_ERR_ARGUMENT, "member capacity too small");
+            PGB_CUDA(cudaMemcpyAsync(member_ids, ctx->members.p, ctx->n_members * sizeof(uint64_t),
+                                     cudaMemcpyDeviceToHost, ctx->st));
+        }
+        PGB_CUDA(cudaStreamSynchronize(ctx->st));
+    });
+}
+
+pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payload_on_device,
+                              uint64_t nsamples, const pgb_chunk_spec* chunks, size_t nchunks,
+                              const pgb_engine_config* cfg, const pgb_link_radii* radii,
+                              size_t* n_candidates, size_t* n_clusters) {
+    return guarded([&] {
+        need(ctx && payload && cfg && radii && (nchunks == 0 || chunks), PGB_ERR_ARGUMENT,
+             "null argument");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        reset_timing(ctx);
+        const uint32_t C = ctx->nchans;
+        const uint8_t* dpay = payload;
+        if (!payload_on_device) {
+            ctx->payload.reserve((size_t)nsamples * C);
+            dpay = ctx->payload.as<uint8_t>();
+            while (ctx->seg_events.size() < nchunks) {
+                cudaEvent_t e;
+                PGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                ctx->seg_events.push_back(e);
+            }
+            // upload segment k = [end of chunk k-1, end of chunk k) on the copy stream
+            uint64_t done = 0;
+            for (size_t k = 0; k < nchunks; ++k) {
+                const uint64_t end = chunks[k].start_sample + chunks[k].length;
+                need(end <= nsamples, PGB_ERR_INVALID_PLAN, "chunk extends past the payload");
+                if (end > done) {
+                    PGB_CUDA(cudaMemcpyAsync(ctx->payload.as<uint8_t>() + done * C, payload + done * C,
+                                             (end - done) * C, cudaMemcpyHostToDevice, ctx->copy_st));
+                    done = end;
+                }
+                PGB_CUDA(cudaEventRecord(ctx->seg_events[k], ctx->copy_st));
+            }
+        }
+        ctx->file_skipped.clear();
+        uint64_t total = 0;
+        std::vector<uint64_t> counts(nchunks);
+        // accumulate per-chunk sorted candidates on the device
+        for (size_t k = 0; k < nchunks; ++k) {
+            validate_cfg(ctx, &chunks[k], cfg);
+            if (!payload_on_device) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
+            run_chunk(ctx, ChunkInput{dpay + chunks[k].start_sample * C, true}, &chunks[k], cfg);
+            const uint64_t nc = ctx->n_cands;
+            if (nc) {
+                if ((total + nc) * sizeof(pgb_candidate) > ctx->file_cands.bytes) {
+                    DevBuf grown;
+                    grown.reserve(std::max<uint64_t>(2 * (total + nc), 4096) * sizeof(pgb_candidate));
+                    if (total)
+                        PGB_CUDA(cudaMemcpyAsync(grown.p, ctx->file_cands.p, total * sizeof(pgb_candidate),
+                                                 cudaMemcpyDeviceToDevice, ctx->st));
+                    PGB_CUDA(cudaStreamSynchronize(ctx->st));
+                    ctx->file_cands.release();
+                    ctx->file_cands = grown;
+                    grown.p = nullptr;
+                }
+                PGB_CUDA(cudaMemcpyAsync(ctx->file_cands.as<pgb_candidate>() + total,
+                                         ctx->cands_sorted.p, nc * sizeof(pgb_candidate),
+                                         cudaMemcpyDeviceToDevice, ctx->st));
+            }
+            total += nc;
+            for (uint64_t t : ctx->skipped) {
+                ctx->file_skipped.push_back(chunks[k].index);
+                ctx->file_skipped.push_back(t);
+            }
+        }
+        // file-level sort (src/pipeline.cpp:100-105) and link_grid (:106)
+        ctx->file_sorted.reserve(std::max<uint64_t>(total, 1) * sizeof(pgb_candidate));
+        if (total) {
+            const size_t tmp = sort_candidates_temp_bytes(total);
+            ctx->sort_tmp.reserve(tmp);
+            ctx->sort_keys.reserve(2 * total * sizeof(uint64_t));
+            ctx->sort_idx.reserve(2 * total * sizeof(uint32_t));
+            sort_candidates(ctx->file_cands.as<pgb_candidate>(), ctx->file_sorted.as<pgb_candidate>(),
+                            total, ctx->sort_tmp.p, tmp, ctx->sort_keys.as<uint64_t>(),
+                            ctx->sort_keys.as<uint64_t>() + total, ctx->sort_idx.as<uint32_t>(),
+                            ctx->sort_idx.as<uint32_t>() + total, ctx->st);
+        }
+        uint64_t ncl = 0;
+        cluster_candidates(ctx->file_sorted.as<pgb_candidate>(), total, *radii, ctx->cl_scratch,
+                           ctx->clusters, ctx->members, &ncl, ctx->st, &ctx->launches);
+        PGB_CUDA(cudaStreamSynchronize(ctx->st));
+        ctx->file_ncands = total;
+        ctx->n_clusters = ncl;
+        ctx->n_members = total;
+        ctx->last_from_file = true;
+        if (n_candidates) *n_candidates = total;
+        if (n_clusters) *n_clusters = ncl;
+    });
+}
+
+pgb_status pgb_fetch_file_candidates(pgb_context* ctx, pgb_candidate* out, size_t capacity) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        need(capacity >= ctx->file_ncands && (ctx->file_ncands == 0 || out), PGB_ERR_ARGUMENT,
+             "capacity too small");
+        if (!ctx->file_ncands) return;
+        PGB_CUDA(cudaMemcpyAsync(out, ctx->file_sorted.p, ctx->file_ncands * sizeof(pgb_candidate),
+                                 cudaMemcpyDeviceToHost, ctx->st));
+        PGB_CUDA(cudaStreamSynchronize(ctx->st));
+    });
+}
+
+pgb_status pgb_fetch_file_skipped(pgb_context* ctx, uint64_t* pairs, size_t capacity, size_t* n_pairs) {
+    return guarded([&] {
+        need(ctx && n_pairs, PGB_ERR_ARGUMENT, "null argument");
+        *n_pairs = ctx->file_skipped.size() / 2;
+        if (!pairs) return;
+        need(capacity >= *n_pairs, PGB_ERR_ARGUMENT, "capacity too small");
+        std::copy(ctx->file_skipped.begin(), ctx->file_skipped.end(), pairs);
+    });
+}
+
+pgb_status pgb_launch_count(pgb_context* ctx, uint64_t* launches) {
+    return guarded([&] {
+        need(ctx && launches, PGB_ERR_ARGUMENT, "null argument");
+        *launches = ctx->launches;
+    });
+}
+
+pgb_status pgb_last_dedisp_time(pgb_context* ctx, double* ms, uint64_t* launches, uint64_t* adds) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        if (ms) *ms = ctx->dedisp_ms;
+        if (launches) *launches = ctx->dedisp_launches;
+        if (adds) *adds = ctx->channel_adds;
+    });
+}
+
+pgb_status pgb_stream(pgb_context* ctx, void** stream) {
+    return guarded([&] {
+        need(ctx && stream, PGB_ERR_ARGUMENT, "null argument");
+        *stream = ctx->st;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,406 @@
+// Brute-force incoherent dedispersion for sm_100a.
+//
+// Semantics: out[t][i] = sum over channels c (ascending) of x[c][i + d_t(c)], the
+// naive definition the reference's single-trial path computes
+// (/root/reference/proj/src/dedisp.cpp:200-218, tests/oracles.hpp:16-26).
+//
+// Layout: the chunk is first transposed to channel-major rows (the reference's
+// transpose_chunk, src/dedisp.cpp:116-131, but on 8-bit codes: 1 byte/cell).
+// A CTA owns a tile of TB consecutive (active) trials x DD_NT consecutive
+// outputs and streams the channels through shared memory G at a time,
+// double-buffered.  For channel c the tile needs the window
+// x[c][i0 + min_t d_t(c) .. i0 + max_t d_t(c) + DD_NT), staged once and read by all
+// TB trials.
+//
+// u8 path (integer, exact): the staged window is stored as four byte-shifted
+// copies so every (trial, channel) reads 4 consecutive samples with one aligned,
+// bank-conflict-free 32-bit LDS.  The 4 bytes are accumulated SWAR-style in two
+// 32-bit registers per word:
+//     E += w & 0x00FF00FF          (samples 0 and 2 in u16 lanes; LOP3 + IADD3)
+//     H += w >> 8  (= mad.hi(w, 2^24, H), samples 1..3 overlapped; fma pipe)
+// which splits the adds across the ALU and FMA pipes.  Every 256 channels the
+// lanes are decoded (B0 = E&0xFFFF, B2 = E>>16, t = H - (B2<<8), B1 = t&0xFFFF,
+// B3 = t>>16; exact because each lane sum < 2^16 and H < 2^32) and added into the
+// int32 output, which stays L2-resident between flushes.  Integer sums of 8-bit
+// codes are exact, and for every north-star config (<= 8192 channels) they are
+// below 2^24, so float(sum) equals the reference's in-order fp32 sum bit for bit.
+//
+// f32 path (non-integer chunks, e.g. after local-mean RFI replacement): the
+// window is staged once with cp.async and every output accumulates the
+// channels in ascending order with IEEE __fadd_rn, reproducing the reference's
+// rounding sequence exactly.
+#include <cuda_pipeline.h>
+
+#include "pgb_internal.h"
+
+namespace pgb {
+
+namespace {
+
+__device__ __forceinline__ uint32_t warp_min_u32(uint32_t v) {
+    for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+__device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(0xffffffffu, v, o));
+    return v;
+}
+
+// Per-stage bookkeeping (phase A): for each staged channel slot, the aligned
+// window start and, per trial, the smem byte/element offset of its first sample.
+// Warp w handles channel slot w (G <= DD_WARPS), lane r trial r of the block.
+template <bool U8, int TB>
+__device__ __forceinline__ void stage_offsets(const DedispLaunch& p, uint32_t c0, int b,
+                                              uint64_t i0, const uint32_t* trial_ids,
+                                              uint64_t* abase, uint32_t* offs) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp >= p.g) return;
+    const uint32_t c = c0 + warp;
+    const bool live = c < p.nchans;
+    uint32_t d = 0;
+    if (live && lane < TB) d = (uint32_t)p.delays_ct[(size_t)c * p.ntrials_plan + trial_ids[lane]];
+    const uint32_t dmin = warp_min_u32(lane < TB ? d : 0xffffffffu);
+    const uint64_t align = U8 ? 16 : 4;  // 16-byte aligned global window start
+    const uint64_t a = (i0 + dmin) & ~(align - 1);
+    const int slot = b * p.g + warp;
+    if (lane == 0) abase[slot] = a;
+    if (lane < TB) {
+        const uint32_t o = (uint32_t)(i0 + d - a);
+        uint32_t off;
+        if (U8) off = (uint32_t)((slot * 4 + (o & 3)) * p.wmax + (o >> 2) * 4);  // byte offset
+        else off = (uint32_t)(slot * p.wmax + o);                               // float index
+        offs[slot * TB + lane] = off;
+    }
+}
+
+constexpr int U8_VPT = 4;  // max 16-byte vectors per thread per stage (host guarantees)
+
+template <int TPW>
+__global__ void __launch_bounds__(DD_THREADS, 1)
+    dedisp_u8_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
+                     int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    constexpr int TB = DD_WARPS * TPW;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int G = p.g;
+    const uint32_t W = p.wmax;  // bytes per copy
+    uint8_t* buf = smem;                                              // [2][G][4][W]
+    uint32_t* offs = reinterpret_cast<uint32_t*>(smem + (size_t)2 * G * 4 * W);  // [2][G][TB]
+    uint64_t* abase = reinterpret_cast<uint64_t*>(offs + 2 * G * TB);            // [2][G]
+    __shared__ uint32_t trial_ids[32];
+
+    const uint32_t blk = blockIdx.y;
+    const uint32_t row0 = blk * TB;
+    const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
+    const uint64_t i0 = (uint64_t)blockIdx.x * DD_NT;
+    if (i0 >= blk_len[blk]) return;  // every trial of the block is shorter than this tile
+    if (threadIdx.x < 32)
+        trial_ids[threadIdx.x] = p.active[row0 + min((uint32_t)threadIdx.x, nrows_blk - 1)];
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nstages = (p.nchans + G - 1) / G;
+    const uint32_t vec_per_ch = W / 16;
+    const uint32_t nvec = (uint32_t)G * vec_per_ch;
+
+    uint4 v0[U8_VPT];
+    uint32_t v1[U8_VPT];
+
+    auto load_stage = [&](uint32_t gi, int b) {
+        const uint32_t c0 = gi * G;
+#pragma unroll
+        for (int k = 0; k < U8_VPT; ++k) {
+            const uint32_t v = threadIdx.x + k * DD_THREADS;
+            if (v < nvec) {
+                const uint32_t cs = v / vec_per_ch, vi = v - cs * vec_per_ch;
+                const uint32_t c = min(c0 + cs, p.nchans - 1);
+                const uint8_t* src = rows + (size_t)c * p.rows_pitch + abase[b * G + cs] + 16 * vi;
+                v0[k] = __ldg(reinterpret_cast<const uint4*>(src));
+                v1[k] = __ldg(reinterpret_cast<const uint32_t*>(src + 16));
+            }
+        }
+    };
+    auto store_stage = [&](int b) {
+#pragma unroll
+        for (int k = 0; k < U8_VPT; ++k) {
+            const uint32_t v = threadIdx.x + k * DD_THREADS;
+            if (v < nvec) {
+                const uint32_t cs = v / vec_per_ch, vi = v - cs * vec_per_ch;
+                uint8_t* dst = buf + (size_t)((b * G + cs) * 4) * W + 16 * vi;
+                const uint32_t w[5] = {v0[k].x, v0[k].y, v0[k].z, v0[k].w, v1[k]};
+                *reinterpret_cast<uint4*>(dst) = v0[k];
+#pragma unroll
+                for (int s = 1; s < 4; ++s) {
+                    const uint32_t sel = (uint32_t)(s | (s + 1) << 4 | (s + 2) << 8 | (s + 3) << 12);
+                    uint4 sh;
+                    sh.x = __byte_perm(w[0], w[1], sel);
+                    sh.y = __byte_perm(w[1], w[2], sel);
+                    sh.z = __byte_perm(w[2], w[3], sel);
+                    sh.w = __byte_perm(w[3], w[4], sel);
+                    *reinterpret_cast<uint4*>(dst + (size_t)s * W) = sh;
+                }
+            }
+        }
+    };
+
+    uint32_t E[TPW][DD_WORDS], H[TPW][DD_WORDS];
+#pragma unroll
+    for (int u = 0; u < TPW; ++u)
+#pragma unroll
+        for (int m = 0; m < DD_WORDS; ++m) E[u][m] = H[u][m] = 0;
+    bool first_flush = true;
+
+    auto flush = [&]() {
+#pragma unroll
+        for (int u = 0; u < TPW; ++u) {
+            const uint32_t r = warp * TPW + u;
+            if (r < nrows_blk) {
+                int32_t* dst = out + (size_t)(row0 + r) * p.out_pitch + i0;
+#pragma unroll
+                for (int m = 0; m < DD_WORDS; ++m) {
+                    const uint32_t q = lane + 32 * m;
+                    const uint32_t e = E[u][m], h = H[u][m];
+                    const uint32_t b0 = e & 0xffffu, b2 = e >> 16;
+                    const uint32_t t = h - (b2 << 8);
+                    int4 val = make_int4((int)b0, (int)(t & 0xffffu), (int)b2, (int)(t >> 16));
+                    int4* pd = reinterpret_cast<int4*>(dst + 4 * q);
+                    if (!first_flush) {
+                        const int4 old = *pd;
+                        val.x += old.x;
+                        val.y += old.y;
+                        val.z += old.z;
+                        val.w += old.w;
+                    }
+                    *pd = val;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < DD_WORDS; ++m) E[u][m] = H[u][m] = 0;
+        }
+        first_flush = false;
+    };
+
+    // prologue: stage 0
+    stage_offsets<true, TB>(p, 0, 0, i0, trial_ids, abase, offs);
+    __syncthreads();
+    load_stage(0, 0);
+    store_stage(0);
+    const uint32_t stages_per_flush = DD_FLUSH_CH / G;
+
+    for (uint32_t gi = 0; gi < nstages; ++gi) {
+        const int b = gi & 1;
+        const bool more = gi + 1 < nstages;
+        if (more) stage_offsets<true, TB>(p, (gi + 1) * G, b ^ 1, i0, trial_ids, abase, offs);
+        __syncthreads();
+        if (more) load_stage(gi + 1, b ^ 1);
+
+        const uint32_t c0 = gi * G;
+        const int nch = (int)min((uint32_t)G, p.nchans - c0);
+        const uint32_t* offb = offs + b * G * TB;
+#pragma unroll 2
+        for (int cs = 0; cs < nch; ++cs) {
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                const uint8_t* src = buf + offb[cs * TB + warp * TPW + u] + 4 * lane;
+#pragma unroll
+                for (int m = 0; m < DD_WORDS; ++m) {
+                    const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 128 * m);
+                    E[u][m] += w & 0x00ff00ffu;
+                    H[u][m] = __umulhi(w, 1u << 24) + H[u][m];
+                }
+            }
+        }
+        if (more) store_stage(b ^ 1);
+        if ((gi + 1) % stages_per_flush == 0 || !more) flush();
+        __syncthreads();
+    }
+}
+
+template <int TPW>
+__global__ void __launch_bounds__(DD_THREADS, 1)
+    dedisp_f32_kernel(const DedispLaunch p, const float* __restrict__ rows,
+                      float* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    constexpr int TB = DD_WARPS * TPW;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int G = p.g;
+    const uint32_t W = p.wmax;  // floats per window
+    float* buf = reinterpret_cast<float*>(smem);                               // [2][G][W]
+    uint32_t* offs = reinterpret_cast<uint32_t*>(smem + (size_t)2 * G * W * 4);  // [2][G][TB]
+    uint64_t* abase = reinterpret_cast<uint64_t*>(offs + 2 * G * TB);
+    __shared__ uint32_t trial_ids[32];
+
+    const uint32_t blk = blockIdx.y;
+    const uint32_t row0 = blk * TB;
+    const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
+    const uint64_t i0 = (uint64_t)blockIdx.x * DD_NT;
+    if (i0 >= blk_len[blk]) return;
+    if (threadIdx.x < 32)
+        trial_ids[threadIdx.x] = p.active[row0 + min((uint32_t)threadIdx.x, nrows_blk - 1)];
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nstages = (p.nchans + G - 1) / G;
+    const uint32_t vec_per_ch = W / 4;
+    const uint32_t nvec = (uint32_t)G * vec_per_ch;
+
+    auto issue_stage = [&](uint32_t gi, int b) {
+        const uint32_t c0 = gi * G;
+        for (uint32_t v = threadIdx.x; v < nvec; v += DD_THREADS) {
+            const uint32_t cs = v / vec_per_ch, vi = v - cs * vec_per_ch;
+            const uint32_t c = min(c0 + cs, p.nchans - 1);
+            const float* src = rows + (size_t)c * p.rows_pitch + abase[b * G + cs] + 4 * vi;
+            __pipeline_memcpy_async(buf + (size_t)(b * G + cs) * W + 4 * vi, src, 16);
+        }
+        __pipeline_commit();
+    };
+
+    float acc[TPW][DD_FOUT];
+#pragma unroll
+    for (int u = 0; u < TPW; ++u)
+#pragma unroll
+        for (int m = 0; m < DD_FOUT; ++m) acc[u][m] = 0.0f;  // the reference starts from +0.0f
+
+    stage_offsets<false, TB>(p, 0, 0, i0, trial_ids, abase, offs);
+    __syncthreads();
+    issue_stage(0, 0);
+
+    for (uint32_t gi = 0; gi < nstages; ++gi) {
+        const int b = gi & 1;
+        const bool more = gi + 1 < nstages;
+        if (more) stage_offsets<false, TB>(p, (gi + 1) * G, b ^ 1, i0, trial_ids, abase, offs);
+        __pipeline_wait_prior(0);
+        __syncthreads();
+        if (more) issue_stage(gi + 1, b ^ 1);
+
+        const uint32_t c0 = gi * G;
+        const int nch = (int)min((uint32_t)G, p.nchans - c0);
+        const uint32_t* offb = offs + b * G * TB;
+        for (int cs = 0; cs < nch; ++cs) {
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                const float* src = buf + offb[cs * TB + warp * TPW + u] + lane;
+#pragma unroll
+                for (int m = 0; m < DD_FOUT; ++m) acc[u][m] = __fadd_rn(acc[u][m], src[32 * m]);
+            }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+        const uint32_t r = warp * TPW + u;
+        if (r < nrows_blk) {
+            float* dst = out + (size_t)(row0 + r) * p.out_pitch + i0;
+#pragma unroll
+            for (int m = 0; m < DD_FOUT; ++m) dst[lane + 32 * m] = acc[u][m];
+        }
+    }
+}
+
+// ---- transposes ---------------------------------------------------------------
+
+// u8 [length][nchans] -> rows [nchans][pitch]; 64x64-byte tiles.
+__global__ void transpose_u8_kernel(const uint8_t* __restrict__ in, uint64_t length,
+                                    uint32_t nchans, uint8_t* __restrict__ rows, uint64_t pitch) {
+    __shared__ uint8_t tile[64][64 + 4];
+    const uint64_t t0 = (uint64_t)blockIdx.x * 64;
+    const uint32_t c0 = blockIdx.y * 64;
+    const int tid = threadIdx.x;
+    const bool full = (t0 + 64 <= length) && (c0 + 64 <= nchans) && (nchans % 16 == 0);
+    if (full) {
+        const int r = tid >> 2, cv = (tid & 3) * 16;
+        const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + (t0 + r) * nchans + c0 + cv));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) *reinterpret_cast<uint32_t*>(&tile[r][cv + 4 * k]) = w[k];
+    } else {
+        for (int k = tid; k < 64 * 64; k += blockDim.x) {
+            const int r = k >> 6, c = k & 63;
+            tile[r][c] = (t0 + r < length && c0 + c < nchans) ? in[(t0 + r) * nchans + c0 + c] : 0;
+        }
+    }
+    __syncthreads();
+    // write: thread -> (channel c, 16 consecutive samples)
+    const int c = tid >> 2, tv = (tid & 3) * 16;
+    if (c0 + c < nchans) {
+        uint32_t w[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+            w[k] = (uint32_t)tile[tv + 4 * k][c] | (uint32_t)tile[tv + 4 * k + 1][c] << 8 |
+                   (uint32_t)tile[tv + 4 * k + 2][c] << 16 | (uint32_t)tile[tv + 4 * k + 3][c] << 24;
+        uint8_t* dst = rows + (uint64_t)(c0 + c) * pitch + t0 + tv;
+        if (t0 + tv + 16 <= pitch)
+            *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
+__global__ void transpose_f32_kernel(const float* __restrict__ in, uint64_t length,
+                                     uint32_t nchans, float* __restrict__ rows, uint64_t pitch) {
+    __shared__ float tile[32][33];
+    const uint64_t t0 = (uint64_t)blockIdx.x * 32;
+    const uint32_t c0 = blockIdx.y * 32;
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    for (int r = ty; r < 32; r += 8) {
+        const uint64_t t = t0 + r;
+        tile[r][tx] = (t < length && c0 + tx < nchans) ? __ldg(in + t * nchans + c0 + tx) : 0.0f;
+    }
+    __syncthreads();
+    for (int r = ty; r < 32; r += 8) {
+        const uint32_t c = c0 + r;
+        if (c < nchans && t0 + tx < pitch) rows[(uint64_t)c * pitch + t0 + tx] = tile[tx][r];
+    }
+}
+
+}  // namespace
+
+size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax) {
+    const int tb = 32;
+    const size_t staged = u8 ? (size_t)2 * g * 4 * wmax : (size_t)2 * g * wmax * 4;
+    return staged + (size_t)2 * g * tb * 4 + (size_t)2 * g * 8;
+}
+
+void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
+    const size_t smem = dedisp_smem_bytes(true, p.g, p.wmax);
+    const int tb = DD_WARPS * p.tpw;
+    dim3 grid(p.ntiles, (p.nrows + tb - 1) / tb);
+    if (p.tpw == 2) {
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_kernel<2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dedisp_u8_kernel<2><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);
+    } else {
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_kernel<1>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dedisp_u8_kernel<1><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);
+    }
+    PGB_CUDA(cudaGetLastError());
+}
+
+void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st) {
+    const size_t smem = dedisp_smem_bytes(false, p.g, p.wmax);
+    const int tb = DD_WARPS * p.tpw;
+    dim3 grid(p.ntiles, (p.nrows + tb - 1) / tb);
+    if (p.tpw == 2) {
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_f32_kernel<2>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dedisp_f32_kernel<2><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);
+    } else {
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_f32_kernel<1>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        dedisp_f32_kernel<1><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);
+    }
+    PGB_CUDA(cudaGetLastError());
+}
+
+void launch_transpose_u8(const uint8_t* in, uint64_t length, uint32_t nchans, uint8_t* rows,
+                         uint64_t pitch, cudaStream_t st) {
+    dim3 grid((unsigned)((length + 63) / 64), (nchans + 63) / 64);
+    transpose_u8_kernel<<<grid, 256, 0, st>>>(in, length, nchans, rows, pitch);
+    PGB_CUDA(cudaGetLastError());
+}
+
+void launch_transpose_f32(const float* in, uint64_t length, uint32_t nchans, float* rows,
+                          uint64_t pitch, cudaStream_t st) {
+    dim3 grid((unsigned)((length + 31) / 32), (nchans + 31) / 32);
+    transpose_f32_kernel<<<grid, 256, 0, st>>>(in, length, nchans, rows, pitch);
+    PGB_CUDA(cudaGetLastError());
+}
+
+}  // namespace pgb

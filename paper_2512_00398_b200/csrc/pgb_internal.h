@@ -1,0 +1,148 @@
+// Internal declarations shared by the CUDA translation units of libpgb200.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/pulsegrid_b200.h"
+
+namespace pgb {
+
+// ---- errors -----------------------------------------------------------------
+
+struct Error {
+    pgb_status code;
+    std::string msg;
+};
+
+[[noreturn]] void raise(pgb_status code, const std::string& msg);
+void check_cuda(cudaError_t e, const char* what);
+#define PGB_CUDA(x) ::pgb::check_cuda((x), #x)
+
+// ---- device buffers (grow-only) -----------------------------------------------
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n, bool zero = false);
+    void release();
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedBuf {
+    void* p = nullptr;
+    size_t bytes = 0;
+    void reserve(size_t n);
+    void release();
+    template <typename T>
+    T* as() const { return static_cast<T*>(p); }
+};
+
+// ---- kernel tiling constants ----------------------------------------------------
+
+// Dedispersion CTA tile: DD_TB trials x DD_NT output samples, 16 warps.
+constexpr int DD_THREADS = 512;
+constexpr int DD_WARPS = DD_THREADS / 32;
+constexpr int DD_NT = 1024;             // outputs per tile
+constexpr int DD_WORDS = DD_NT / 128;   // u8 path: 4-byte words per lane per trial (8)
+constexpr int DD_FOUT = DD_NT / 32;     // f32 path: outputs per lane per trial (32)
+constexpr int DD_FLUSH_CH = 256;        // u16-lane SWAR accumulators flush period (channels)
+constexpr size_t DD_SMEM_BUDGET = 200 * 1024;
+
+// Boxcar/peak CTA: buffer of BX_N doubles, BX_THREADS threads.
+constexpr int BX_THREADS = 512;
+
+// Packed fragment of an above-threshold run that touches a strip edge.
+struct Fragment {
+    uint64_t key;      // row << 40 | level << 35 | begin  (sort key)
+    uint32_t row;      // active-trial row
+    uint32_t level;    // width index
+    uint64_t begin;    // series index, inclusive
+    uint64_t end;      // series index, inclusive
+    uint64_t peak;     // series index of first maximum
+    double peak_v;     // sums[peak] * scale
+};
+
+// Per-run parameters of the chain kernels.
+struct ChainParams {
+    uint64_t start_sample;
+    uint64_t valid_begin;
+    uint64_t valid_end;
+    int drop_left;
+    int drop_right;
+    double tsamp;
+    double threshold;   // double(detect_thresh)
+    uint64_t boxcar_max;
+    uint64_t window;    // baseline window (forced odd), 0 = off
+};
+
+// ---- launchers (defined in the .cu files; all asynchronous on `st`) ------------
+
+// u8 [length][nchans] -> rows [nchans][pitch]
+void launch_transpose_u8(const uint8_t* in, uint64_t length, uint32_t nchans, uint8_t* rows,
+                         uint64_t pitch, cudaStream_t st);
+void launch_transpose_f32(const float* in, uint64_t length, uint32_t nchans, float* rows,
+                          uint64_t pitch, cudaStream_t st);
+
+struct DedispLaunch {
+    const int32_t* delays_ct;   // [nchans][ntrials_plan] int32
+    uint32_t ntrials_plan;
+    uint32_t nchans;
+    const uint32_t* active;     // [nrows] plan trial ids
+    uint32_t nrows;
+    const uint32_t* row_len;    // [nrows] series length n_t
+    const uint32_t* blk_len;    // [nblocks] longest series of each trial block
+    uint64_t rows_pitch;        // elements per channel row
+    uint64_t out_pitch;         // elements per output row
+    int tpw;                    // trials per warp (2 -> 32-trial blocks, 1 -> 16)
+    int g;                      // channels per stage
+    uint32_t wmax;              // staged window length (elements)
+    uint32_t ntiles;            // time tiles (grid.x)
+};
+void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st);
+void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st);
+size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax);
+
+// chain
+void launch_baseline_int(const int32_t* x, float* out, const uint32_t* row_len, uint32_t nrows,
+                         uint64_t pitch, uint64_t window, cudaStream_t st);
+void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, uint32_t nrows,
+                         uint64_t pitch, uint64_t window, cudaStream_t st);
+// input kind: 0 = float baseline output, 1 = int32 series, 2 = float series
+void launch_rms(const void* x, int kind, const uint32_t* row_len, uint32_t nrows, uint64_t pitch,
+                float* frms, uint8_t* status, cudaStream_t st);
+void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const float* frms,
+                         const uint8_t* status, uint32_t nrows, uint64_t pitch,
+                         uint64_t max_len, const ChainParams& cp, const uint32_t* active,
+                         const double* dms, const double* scale, pgb_candidate* cands, unsigned long long* n_cands,
+                         uint64_t cand_cap, Fragment* frags, unsigned long long* n_frags,
+                         uint64_t frag_cap, cudaStream_t st);
+void launch_stitch(const Fragment* frags_sorted, uint64_t nfrags, const uint32_t* row_len,
+                   const ChainParams& cp, const uint32_t* active, const double* dms,
+                   pgb_candidate* cands, unsigned long long* n_cands, uint64_t cand_cap,
+                   cudaStream_t st);
+
+// sorting helpers (CUB)
+size_t sort_fragments_temp_bytes(uint64_t n);
+void sort_fragments(Fragment* frags, Fragment* tmp, uint64_t n, void* temp, size_t temp_bytes,
+                    uint64_t* keys_a, uint64_t* keys_b, uint32_t* idx_a, uint32_t* idx_b,
+                    cudaStream_t st);
+size_t sort_candidates_temp_bytes(uint64_t n);
+void sort_candidates(const pgb_candidate* in, pgb_candidate* out, uint64_t n, void* temp,
+                     size_t temp_bytes, uint64_t* keys_a, uint64_t* keys_b, uint32_t* idx_a,
+                     uint32_t* idx_b, cudaStream_t st);
+
+// clustering
+struct ClusterWork;  // device scratch, defined in cluster.cu
+struct ClusterResultDev {
+    uint64_t nclusters = 0;
+};
+void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_radii& radii,
+                        DevBuf& scratch, DevBuf& out_clusters, DevBuf& out_members,
+                        uint64_t* nclusters, cudaStream_t st, uint64_t* launches);
+
+}  // namespace pgb

@@ -1,0 +1,379 @@
+"""The DM loop: pulsegrid's engine.hpp API on the B200.
+
+`run_dm_loop(chunk, plan, cfg)` is the drop-in for
+pulsegrid::run_dm_loop (/root/reference/proj/include/pulsegrid/engine.hpp:61-62,
+src/engine.cpp:85-265): same inputs (a time-major chunk with its ChunkSpec, the
+DM plan, the engine config), same output (candidates sorted by
+(peak_sample, dm_trial, width_index) plus the sorted skipped trials), same
+exceptions.  The work runs in libpgb200 on one CUDA device; there is no CPU path.
+
+Differences that are deliberate and documented in DESIGN.md:
+* n_workers / memory_budget / max_in_flight are validated like the reference but
+  do not change how the device batches trials (results never depended on them);
+* the BufferPool argument is accepted and ignored: device memory comes from the
+  engine's own arena.
+"""
+from __future__ import annotations
+
+import ctypes
+import threading
+from dataclasses import dataclass, field
+from typing import Callable
+
+import numpy as np
+
+from . import abi
+from ._native import check, lib
+from .dedisp import DmTrialPlan
+
+
+@dataclass
+class ChunkSpec:
+    """pulsegrid::ChunkSpec (filterbank.hpp:48-55)."""
+
+    index: int = 0
+    start_sample: int = 0
+    length: int = 0
+    overlap: int = 0
+    valid_begin: int = 0
+    valid_end: int = 0
+
+    def _c(self) -> abi.ChunkSpecC:
+        return abi.ChunkSpecC(self.index, self.start_sample, self.length, self.overlap,
+                              self.valid_begin, self.valid_end)
+
+    @staticmethod
+    def whole(length: int, start: int = 0) -> "ChunkSpec":
+        """The spec tests/oracles.hpp:make_chunk builds (valid range = the chunk)."""
+        return ChunkSpec(0, start, length, 0, start, start + length)
+
+
+@dataclass
+class Chunk:
+    """pulsegrid::Chunk (filterbank.hpp:59-67): time-major [length][nchans] samples.
+
+    `data` may be uint8 codes (the raw 8-bit payload -- exact integer path), float32
+    (widened samples; exact in-order fp32 path), or a CUDA torch tensor of either
+    dtype already resident on the engine's device.
+    """
+
+    spec: ChunkSpec
+    data: object
+
+    @property
+    def nchans(self) -> int:
+        return int(self.data.shape[1])
+
+
+@dataclass
+class LinkRadii:
+    """pulsegrid::LinkRadii (cluster.hpp:13-17)."""
+
+    sep_time: int = 3
+    sep_dm_trials: int = 9
+    sep_width: int = 3
+
+    def _c(self) -> abi.LinkRadiiC:
+        return abi.LinkRadiiC(self.sep_time, self.sep_dm_trials, self.sep_width)
+
+
+@dataclass
+class TrialTiming:
+    """pulsegrid::TrialTiming (engine.hpp:16-23); device stages are amortized per trial."""
+
+    trial: int = 0
+    dedisperse_ms: float = 0.0
+    baseline_ms: float = 0.0
+    normalize_ms: float = 0.0
+    boxcar_ms: float = 0.0
+    peaks_ms: float = 0.0
+
+
+@dataclass
+class EngineConfig:
+    """pulsegrid::EngineConfig (engine.hpp:25-35)."""
+
+    n_workers: int = 1
+    tsamp: float = 0.0
+    detect_thresh: float = 6.0
+    boxcar_max: int = 4096
+    baseline_window: int = 0
+    radii: LinkRadii = field(default_factory=LinkRadii)
+    memory_budget: int = 2 << 30
+    max_in_flight: int = 0
+    timing_sink: Callable[[TrialTiming], None] | None = None
+
+    def _c(self) -> abi.EngineConfigC:
+        return abi.EngineConfigC(int(self.n_workers), float(self.detect_thresh), float(self.tsamp),
+                                 int(self.boxcar_max), int(self.baseline_window),
+                                 int(self.memory_budget), int(self.max_in_flight))
+
+
+@dataclass
+class DmLoopResult:
+    """pulsegrid::DmLoopResult (engine.hpp:37-40), as numpy arrays."""
+
+    candidates: np.ndarray       # abi.CANDIDATE_DTYPE, sorted by (peak, trial, width)
+    skipped_trials: np.ndarray   # uint64, ascending
+
+
+def partition_trials(ntrials: int, n_workers: int) -> list[list[int]]:
+    """src/engine.cpp:53-58 (kept for API parity; the device does not partition)."""
+    parts: list[list[int]] = [[] for _ in range(max(1, n_workers))]
+    for i in range(ntrials):
+        parts[i % len(parts)].append(i)
+    return parts
+
+
+def _aligned(n: int) -> int:
+    v = max(n, 256)
+    return 1 << (v - 1).bit_length()
+
+
+def trial_working_set_bytes(plan: DmTrialPlan, chunk_len: int, cfg: EngineConfig) -> int:
+    """src/engine.cpp:60-73."""
+    min_delay = plan.trial_max_delay(0)
+    longest = chunk_len - min_delay if chunk_len > min_delay else 1
+    series = _aligned(longest * 4)
+    n_blocks = (longest + 63) // 64
+    sums = _aligned((longest + n_blocks) * 8)
+    return (2 if cfg.baseline_window > 0 else 1) * series + sums
+
+
+def in_flight_limit(plan: DmTrialPlan, chunk_len: int, cfg: EngineConfig) -> int:
+    """src/engine.cpp:75-83."""
+    from .errors import ConfigError
+
+    ws = trial_working_set_bytes(plan, chunk_len, cfg)
+    limit = cfg.memory_budget // ws
+    if limit == 0:
+        raise ConfigError(f"memory budget of {cfg.memory_budget} bytes is below one trial's "
+                          f"working set ({ws})")
+    return limit
+
+
+def _device_tensor(x):
+    """(data_ptr, is_u8, device) for a CUDA torch tensor, else None."""
+    try:
+        import torch
+    except ImportError:  # pragma: no cover
+        return None
+    if isinstance(x, torch.Tensor):
+        if not x.is_cuda:
+            return None
+        if not x.is_contiguous():
+            raise ValueError("device chunk must be contiguous")
+        if x.dtype not in (torch.uint8, torch.float32):
+            raise TypeError("device chunk must be uint8 or float32")
+        return x.data_ptr(), x.dtype == torch.uint8, x.device.index or 0
+    return None
+
+
+class Engine:
+    """One libpgb200 context: a CUDA stream plus a device arena on one GPU."""
+
+    def __init__(self, device: int = 0):
+        self.device = device
+        h = ctypes.c_void_p()
+        check(lib.pgb_create(int(device), ctypes.byref(h)))
+        self._h = h
+        self._plan_key = None
+        self._range = None
+
+    # ---- lifecycle -----------------------------------------------------------
+    def close(self) -> None:
+        if self._h:
+            lib.pgb_destroy(self._h)
+            self._h = None
+
+    def __del__(self):  # pragma: no cover - interpreter teardown order
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    # ---- plan ------------------------------------------------------------------
+    def set_plan(self, plan: DmTrialPlan, trial_range: tuple[int, int] | None = None) -> None:
+        key = (id(plan), plan.ntrials, plan.nchans, plan.delays.ctypes.data)
+        if key != self._plan_key:
+            check(lib.pgb_set_plan(self._h, abi.ptr(plan.dms), abi.ptr(plan.delays),
+                                   plan.ntrials, plan.nchans))
+            self._plan_key = key
+            self._plan_ref = plan  # keep the arrays alive while the key is cached
+            self._range = None
+        rng = trial_range if trial_range is not None else (0, plan.ntrials)
+        if rng != self._range:
+            check(lib.pgb_set_trial_range(self._h, int(rng[0]), int(rng[1])))
+            self._range = rng
+
+    # ---- run_dm_loop -------------------------------------------------------------
+    def run_dm_loop(self, chunk: Chunk, plan: DmTrialPlan, cfg: EngineConfig,
+                    pool=None, *, trial_range: tuple[int, int] | None = None) -> DmLoopResult:
+        del pool  # device arena replaces the host BufferPool
+        self.set_plan(plan, trial_range)
+        spec = chunk.spec._c()
+        ccfg = cfg._c()
+        nc, ns = ctypes.c_size_t(), ctypes.c_size_t()
+        dev = _device_tensor(chunk.data)
+        if dev is not None:
+            ptr, is_u8, _ = dev
+            import torch
+
+            torch.cuda.current_stream().synchronize()
+            fn = lib.pgb_run_dm_loop_u8 if is_u8 else lib.pgb_run_dm_loop_f32
+            check(fn(self._h, ctypes.c_void_p(ptr), 1, ctypes.byref(spec), ctypes.byref(ccfg),
+                     ctypes.byref(nc), ctypes.byref(ns)))
+        else:
+            data = np.asarray(chunk.data)
+            if data.ndim != 2 or data.shape[1] != plan.nchans:
+                raise ValueError("chunk data must be [length][nchans] matching the plan")
+            if data.shape[0] < chunk.spec.length:
+                raise ValueError("chunk data shorter than spec.length")
+            if data.dtype == np.uint8:
+                data = np.ascontiguousarray(data)
+                fn = lib.pgb_run_dm_loop_u8
+            else:
+                data = np.ascontiguousarray(data, dtype=np.float32)
+                fn = lib.pgb_run_dm_loop_f32
+            check(fn(self._h, abi.ptr(data), 0, ctypes.byref(spec), ctypes.byref(ccfg),
+                     ctypes.byref(nc), ctypes.byref(ns)))
+        cands = np.zeros(nc.value, abi.CANDIDATE_DTYPE)
+        check(lib.pgb_fetch_candidates(self._h, abi.ptr(cands), nc.value))
+        skipped = np.zeros(ns.value, np.uint64)
+        check(lib.pgb_fetch_skipped(self._h, abi.ptr(skipped), ns.value))
+        if cfg.timing_sink is not None:
+            ms, _, _ = self.last_dedisp_time()
+            lo, hi = self._range
+            per = ms / max(1, hi - lo)
+            for t in range(lo, hi):
+                cfg.timing_sink(TrialTiming(trial=t, dedisperse_ms=per))
+        return DmLoopResult(cands, skipped)
+
+    # ---- dedispersion only --------------------------------------------------------
+    def dedisperse(self, chunk_data: np.ndarray, plan: DmTrialPlan, trials: range | None = None
+                   ) -> list[np.ndarray]:
+        """Dedispersed series of trials [b, e) (dedisperse/dedisperse_block semantics)."""
+        self.set_plan(plan)
+        data = np.asarray(chunk_data)
+        L = data.shape[0]
+        b, e = (0, plan.ntrials) if trials is None else (trials.start, trials.stop)
+        out = np.zeros((max(0, e - b), L), np.float32)
+        if data.dtype == np.uint8:
+            data = np.ascontiguousarray(data)
+            fn = lib.pgb_dedisperse_u8
+        else:
+            data = np.ascontiguousarray(data, dtype=np.float32)
+            fn = lib.pgb_dedisperse_f32
+        check(fn(self._h, abi.ptr(data), L, b, e, abi.ptr(out), L))
+        return [out[r, : L - plan.trial_max_delay(b + r)] for r in range(e - b)]
+
+    # ---- link_grid ----------------------------------------------------------------
+    def link_grid(self, cands, radii: LinkRadii | None = None) -> "Clusters":
+        from .cluster import Clusters
+
+        radii = radii or LinkRadii()
+        r = radii._c()
+        n = ctypes.c_size_t()
+        dev = _device_tensor(cands) if not isinstance(cands, np.ndarray) else None
+        if dev is not None:
+            raise TypeError("pass device candidates through Engine.link_device()")
+        arr = np.ascontiguousarray(cands, abi.CANDIDATE_DTYPE)
+        check(lib.pgb_link_grid(self._h, abi.ptr(arr), 0, len(arr), ctypes.byref(r), ctypes.byref(n)))
+        return self._fetch_clusters(n.value, len(arr))
+
+    def link_last(self, radii: LinkRadii | None = None) -> "Clusters":
+        """link_grid on the last run's device-resident candidates (no round trip)."""
+        radii = radii or LinkRadii()
+        r = radii._c()
+        p, cnt, n = ctypes.c_void_p(), ctypes.c_size_t(), ctypes.c_size_t()
+        check(lib.pgb_device_candidates(self._h, ctypes.byref(p), ctypes.byref(cnt)))
+        check(lib.pgb_link_grid(self._h, p, 1, cnt.value, ctypes.byref(r), ctypes.byref(n)))
+        return self._fetch_clusters(n.value, cnt.value)
+
+    def _fetch_clusters(self, ncl: int, nmem: int) -> "Clusters":
+        from .cluster import Clusters
+
+        recs = np.zeros(ncl, abi.CLUSTER_DTYPE)
+        members = np.zeros(nmem, np.uint64)
+        check(lib.pgb_fetch_clusters(self._h, abi.ptr(recs), ncl, abi.ptr(members), nmem))
+        return Clusters(recs, members)
+
+    # ---- file-level search ------------------------------------------------------------
+    def search_file(self, payload, nsamples: int, chunks: list[ChunkSpec], plan: DmTrialPlan,
+                    cfg: EngineConfig, *, trial_range: tuple[int, int] | None = None):
+        """execute_task's chunk loop + sort + link_grid on a raw 8-bit payload.
+
+        Returns (candidates, clusters, skipped (chunk, trial) pairs)."""
+        self.set_plan(plan, trial_range)
+        arr = np.zeros(len(chunks), abi.CHUNK_SPEC_DTYPE)
+        for k, c in enumerate(chunks):
+            arr[k] = (c.index, c.start_sample, c.length, c.overlap, c.valid_begin, c.valid_end)
+        ccfg = cfg._c()
+        r = cfg.radii._c()
+        nc, ncl = ctypes.c_size_t(), ctypes.c_size_t()
+        dev = _device_tensor(payload)
+        if dev is not None:
+            import torch
+
+            torch.cuda.current_stream().synchronize()
+            ptr, on_dev = ctypes.c_void_p(dev[0]), 1
+        else:
+            payload = np.ascontiguousarray(payload, dtype=np.uint8)
+            ptr, on_dev = abi.ptr(payload), 0
+        check(lib.pgb_search_file_u8(self._h, ptr, on_dev, int(nsamples), abi.ptr(arr), len(arr),
+                                     ctypes.byref(ccfg), ctypes.byref(r), ctypes.byref(nc),
+                                     ctypes.byref(ncl)))
+        return self.fetch_file_results(nc.value, ncl.value)
+
+    def fetch_file_results(self, nc: int, ncl: int):
+        cands = np.zeros(nc, abi.CANDIDATE_DTYPE)
+        check(lib.pgb_fetch_file_candidates(self._h, abi.ptr(cands), nc))
+        clusters = self._fetch_clusters(ncl, nc)
+        npairs = ctypes.c_size_t()
+        check(lib.pgb_fetch_file_skipped(self._h, None, 0, ctypes.byref(npairs)))
+        pairs = np.zeros((npairs.value, 2), np.uint64)
+        check(lib.pgb_fetch_file_skipped(self._h, abi.ptr(pairs), npairs.value, ctypes.byref(npairs)))
+        return cands, clusters, pairs
+
+    # ---- instrumentation ------------------------------------------------------------------
+    def launch_count(self) -> int:
+        v = ctypes.c_uint64()
+        check(lib.pgb_launch_count(self._h, ctypes.byref(v)))
+        return v.value
+
+    def last_dedisp_time(self) -> tuple[float, int, int]:
+        ms, n, adds = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.pgb_last_dedisp_time(self._h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(adds)))
+        return ms.value, n.value, adds.value
+
+    def stream_handle(self) -> int:
+        p = ctypes.c_void_p()
+        check(lib.pgb_stream(self._h, ctypes.byref(p)))
+        return p.value or 0
+
+
+_engines: dict[tuple[int, int], Engine] = {}
+_lock = threading.Lock()
+
+
+def default_engine(device: int = 0) -> Engine:
+    """One engine per (thread, device): run_dm_loop is re-entrant across threads like the
+    reference's (src/pipeline.cpp:182-194)."""
+    key = (threading.get_ident(), device)
+    with _lock:
+        eng = _engines.get(key)
+        if eng is None:
+            eng = _engines[key] = Engine(device)
+        return eng
+
+
+def run_dm_loop(chunk: Chunk, plan: DmTrialPlan, cfg: EngineConfig, pool=None, *,
+                device: int = 0) -> DmLoopResult:
+    """pulsegrid::run_dm_loop (engine.hpp:61-62) on the B200."""
+    return default_engine(device).run_dm_loop(chunk, plan, cfg, pool)
