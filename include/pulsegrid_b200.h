@@ -189,7 +189,8 @@ pgb_status pgb_fetch_clusters(pgb_context* ctx, pgb_cluster* out, size_t capacit
  * overlaps the previous chunk's compute) or, with payload_on_device != 0, already
  * resident in device memory.  Runs every chunk of `chunks` (plan_chunks output) with
  * double-buffered H2D, accumulates candidates on the device, sorts them and
- * clusters them with link_grid.  Fetch with pgb_fetch_clusters /
+ * clusters them with link_grid (radii == NULL: stop after the sorted candidates, as a
+ * multi-GPU trial shard does before the candidate gather).  Fetch with pgb_fetch_clusters /
  * pgb_fetch_file_candidates / pgb_fetch_file_skipped. */
 pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payload_on_device,
                               uint64_t nsamples, const pgb_chunk_spec* chunks, size_t nchunks,
@@ -210,6 +211,10 @@ pgb_status pgb_last_dedisp_time(pgb_context* ctx, double* ms, uint64_t* launches
                                 uint64_t* channel_adds);
 /* The context's CUDA stream (cudaStream_t), for callers that order their own work. */
 pgb_status pgb_stream(pgb_context* ctx, void** stream);
+/* Measured CUDA-core 32-bit add throughput of `device` (lane-adds/s): the roofline
+ * denominator of the ALU-bound dedispersion kernel.  per_mode (optional, [3]):
+ * integer-only, fp32-only, interleaved. */
+pgb_status pgb_microbench_add_peak(int device, double* adds_per_s, double* per_mode);
 
 #ifdef __cplusplus
 }

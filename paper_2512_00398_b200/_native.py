@@ -57,6 +57,7 @@ SIGNATURES = {
     "pgb_launch_count": ([_vp, _P(_u64)], _int),
     "pgb_last_dedisp_time": ([_vp, _P(_c.c_double), _P(_u64), _P(_u64)], _int),
     "pgb_stream": ([_vp, _P(_vp)], _int),
+    "pgb_microbench_add_peak": ([_int, _P(_c.c_double), _vp], _int),
 }
 
 for _name, (_args, _res) in SIGNATURES.items():

@@ -308,6 +308,7 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     dl.g = g;
     dl.wmax = wmax;
     dl.ntiles = ntiles;
+    dl.mul24 = 1u << 24;
     PGB_CUDA(cudaEventRecord(ctx->ev_dd0, st));
     if (u8) launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
     else launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
@@ -766,7 +767,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                               const pgb_engine_config* cfg, const pgb_link_radii* radii,
                               size_t* n_candidates, size_t* n_clusters) {
     return guarded([&] {
-        need(ctx && payload && cfg && radii && (nchunks == 0 || chunks), PGB_ERR_ARGUMENT,
+        need(ctx && payload && cfg && (nchunks == 0 || chunks), PGB_ERR_ARGUMENT,
              "null argument");
         PGB_CUDA(cudaSetDevice(ctx->device));
         reset_timing(ctx);
@@ -837,12 +838,13 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                             ctx->sort_idx.as<uint32_t>() + total, ctx->st);
         }
         uint64_t ncl = 0;
-        cluster_candidates(ctx->file_sorted.as<pgb_candidate>(), total, *radii, ctx->cl_scratch,
-                           ctx->clusters, ctx->members, &ncl, ctx->st, &ctx->launches);
+        if (radii)  // radii == NULL: candidates only (multi-GPU shards cluster after the gather)
+            cluster_candidates(ctx->file_sorted.as<pgb_candidate>(), total, *radii, ctx->cl_scratch,
+                               ctx->clusters, ctx->members, &ncl, ctx->st, &ctx->launches);
         PGB_CUDA(cudaStreamSynchronize(ctx->st));
         ctx->file_ncands = total;
         ctx->n_clusters = ncl;
-        ctx->n_members = total;
+        ctx->n_members = radii ? total : 0;
         ctx->last_from_file = true;
         if (n_candidates) *n_candidates = total;
         if (n_clusters) *n_clusters = ncl;

@@ -17,6 +17,8 @@
 //     maximum of each run, edge-run and valid-range filters.  Runs fully inside one
 //     thread strip are emitted directly; runs touching a strip edge become fragments
 //     that a second kernel stitches after a device sort.
+#include <cuda_pipeline.h>
+
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -172,99 +174,133 @@ __device__ __forceinline__ float load_x(const void* base, size_t idx) {
     return static_cast<const float*>(base)[idx];
 }
 
+// One warp = 8 trials x 4 chains.  The chains are strictly sequential (the
+// reference's rounding order), so the kernel's job is to keep each chain's DADD
+// dependency fed: the 8 rows stream through a 4-stage cp.async ring in shared
+// memory (rows padded by 4 floats so the 32 lanes hit 32 banks), and each lane
+// reads 16 values ahead of its add chain.  Both passes (sum of squares, then the
+// 3-sigma-clipped sum) run in the same kernel.
+constexpr int RMS_TR = 8;          // trials per block
+constexpr int RMS_T = 1024;        // elements per trial per stage
+constexpr int RMS_LD = RMS_T + 4;  // padded row length (floats)
+constexpr int RMS_NST = 4;         // ring stages
+
 template <int KIND>
-__global__ void rms_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len,
-                           uint32_t nrows, uint64_t pitch, float* __restrict__ frms,
-                           uint8_t* __restrict__ status) {
-    const uint32_t gt = blockIdx.x * blockDim.x + threadIdx.x;
-    const uint32_t row = gt >> 2;
-    const int k = gt & 3;
+__global__ void __launch_bounds__(32)
+    rms_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len, uint32_t nrows,
+               uint64_t pitch, float* __restrict__ frms, uint8_t* __restrict__ status) {
+    extern __shared__ __align__(16) float rsm[];  // [RMS_NST][RMS_TR][RMS_LD]
+    const int lane = threadIdx.x, tr = lane >> 2, k = lane & 3;
+    const uint32_t row0 = blockIdx.x * RMS_TR;
+    const uint32_t row = row0 + tr;
     const bool live = row < nrows;
     const uint64_t n = live ? row_len[row] : 0;
-    const size_t base = (size_t)(live ? row : 0) * pitch;
-    const uint64_t nq = n / 4;  // full groups of 4
+    const uint64_t nq4 = n & ~3ull;  // elements covered by the 4-chain loop
+    uint64_t nmax = n;
+    for (int o = 16; o; o >>= 1) nmax = max(nmax, (uint64_t)__shfl_xor_sync(0xffffffffu, nmax, o));
+    const uint64_t nstages = (nmax + RMS_T - 1) / RMS_T;
+    const char* base = static_cast<const char*>(x_all);
 
-    // pass 1: a_k = sum over i = 4j + k of x^2, tail into chain 0
-    double a = 0.0;
-    {
-        uint64_t j = 0;
-        for (; j + 8 <= nq; j += 8) {
-            float v[8];
-#pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = load_x<KIND>(x_all, base + 4 * (j + u) + k);
-#pragma unroll
-            for (int u = 0; u < 8; ++u) a = __dadd_rn(a, __dmul_rn((double)v[u], (double)v[u]));
-        }
-        for (; j < nq; ++j) {
-            const float v = load_x<KIND>(x_all, base + 4 * j + k);
-            a = __dadd_rn(a, __dmul_rn((double)v, (double)v));
-        }
-        if (k == 0)
-            for (uint64_t i = 4 * nq; i < n; ++i) {
-                const float v = load_x<KIND>(x_all, base + i);
-                a = __dadd_rn(a, __dmul_rn((double)v, (double)v));
+    auto issue = [&](uint64_t st) {
+        if (st < nstages) {
+            float* dst = rsm + (st % RMS_NST) * RMS_TR * RMS_LD;
+            for (int v = lane; v < RMS_TR * (RMS_T / 4); v += 32) {
+                const int r = v / (RMS_T / 4), e4 = v % (RMS_T / 4);
+                const uint32_t rr = min(row0 + r, nrows - 1);
+                const char* src = base + ((size_t)rr * pitch + st * RMS_T + 4 * e4) * 4;
+                __pipeline_memcpy_async(dst + r * RMS_LD + 4 * e4, src, 16);
             }
-    }
-    const unsigned mask = 0xffffffffu;
-    const double a1 = __shfl_down_sync(mask, a, 1, 4);
-    const double a2 = __shfl_down_sync(mask, a, 2, 4);
-    const double a3 = __shfl_down_sync(mask, a, 3, 4);
-    double sumsq = __dadd_rn(__dadd_rn(a, a1), __dadd_rn(a2, a3));  // valid on k == 0
-    sumsq = __shfl_sync(mask, sumsq, 0, 4);
-    const double rms0 = __dsqrt_rn(__ddiv_rn(sumsq, (double)n));
-    const float cut = __double2float_rn(__dmul_rn(3.0, rms0));
+        }
+        __pipeline_commit();
+    };
 
-    // pass 2: |x| <= cut
-    double b = 0.0;
+    double a = 0.0, b = 0.0;
     unsigned long long kept = 0;
-    {
-        uint64_t j = 0;
-        for (; j + 8 <= nq; j += 8) {
-            float v[8];
+    float cut = 0.0f;
+    double rms0 = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+        for (int st = 0; st < RMS_NST - 1; ++st) issue(st);
+        for (uint64_t st = 0; st < nstages; ++st) {
+            issue(st + RMS_NST - 1);
+            __pipeline_wait_prior(RMS_NST - 1);
+            __syncwarp();
+            const float* t = rsm + (st % RMS_NST) * RMS_TR * RMS_LD + tr * RMS_LD;
+            const uint64_t i0 = st * RMS_T;
+            const int jmax = nq4 > i0 ? (int)min((uint64_t)RMS_T, nq4 - i0) : 0;
+            int j = k;
+            for (; j + 60 < jmax; j += 64) {  // 16 values ahead of the add chain
+                float v[16];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) v[u] = load_x<KIND>(x_all, base + 4 * (j + u) + k);
+                for (int u = 0; u < 16; ++u) {
+                    const float f = t[j + 4 * u];
+                    v[u] = KIND == 1 ? (float)__float_as_int(f) : f;
+                }
 #pragma unroll
-            for (int u = 0; u < 8; ++u)
-                if (fabsf(v[u]) <= cut) {
-                    b = __dadd_rn(b, __dmul_rn((double)v[u], (double)v[u]));
+                for (int u = 0; u < 16; ++u) {
+                    const double sq = __dmul_rn((double)v[u], (double)v[u]);
+                    if (pass == 0) {
+                        a = __dadd_rn(a, sq);
+                    } else if (fabsf(v[u]) <= cut) {
+                        b = __dadd_rn(b, sq);
+                        ++kept;
+                    }
+                }
+            }
+            for (; j < jmax; j += 4) {
+                const float f = t[j];
+                const float vv = KIND == 1 ? (float)__float_as_int(f) : f;
+                const double sq = __dmul_rn((double)vv, (double)vv);
+                if (pass == 0) {
+                    a = __dadd_rn(a, sq);
+                } else if (fabsf(vv) <= cut) {
+                    b = __dadd_rn(b, sq);
                     ++kept;
                 }
-        }
-        for (; j < nq; ++j) {
-            const float v = load_x<KIND>(x_all, base + 4 * j + k);
-            if (fabsf(v) <= cut) {
-                b = __dadd_rn(b, __dmul_rn((double)v, (double)v));
-                ++kept;
             }
+            __syncwarp();
         }
-        if (k == 0)
-            for (uint64_t i = 4 * nq; i < n; ++i) {
-                const float v = load_x<KIND>(x_all, base + i);
-                if (fabsf(v) <= cut) {
-                    b = __dadd_rn(b, __dmul_rn((double)v, (double)v));
+        __pipeline_wait_prior(0);
+        // tail (< 4 elements) into chain 0, src/detect.cpp:76 / :100-105
+        if (k == 0 && live)
+            for (uint64_t i = nq4; i < n; ++i) {
+                const size_t idx = (size_t)row * pitch + i;
+                const float vv = KIND == 1 ? (float)static_cast<const int32_t*>(x_all)[idx]
+                                           : static_cast<const float*>(x_all)[idx];
+                const double sq = __dmul_rn((double)vv, (double)vv);
+                if (pass == 0) {
+                    a = __dadd_rn(a, sq);
+                } else if (fabsf(vv) <= cut) {
+                    b = __dadd_rn(b, sq);
                     ++kept;
                 }
             }
-    }
-    const double b1 = __shfl_down_sync(mask, b, 1, 4);
-    const double b2 = __shfl_down_sync(mask, b, 2, 4);
-    const double b3 = __shfl_down_sync(mask, b, 3, 4);
-    unsigned long long kt = kept;
-    kt += __shfl_down_sync(mask, kept, 1, 4);
-    kt += __shfl_down_sync(mask, kept, 2, 4);
-    kt += __shfl_down_sync(mask, kept, 3, 4);
-    if (live && k == 0) {
-        const double kept_sumsq = __dadd_rn(__dadd_rn(b, b1), __dadd_rn(b2, b3));
-        uint8_t st = 0;
-        double rms = rms0;
-        if (n < 2 || rms0 == 0.0) {
-            st = 1;
+        const double x = pass == 0 ? a : b;
+        const double x1 = __shfl_down_sync(0xffffffffu, x, 1, 4);
+        const double x2 = __shfl_down_sync(0xffffffffu, x, 2, 4);
+        const double x3 = __shfl_down_sync(0xffffffffu, x, 3, 4);
+        double tot = __dadd_rn(__dadd_rn(x, x1), __dadd_rn(x2, x3));  // (a0+a1)+(a2+a3)
+        tot = __shfl_sync(0xffffffffu, tot, lane & ~3);
+        if (pass == 0) {
+            rms0 = __dsqrt_rn(__ddiv_rn(tot, (double)n));
+            cut = __double2float_rn(__dmul_rn(3.0, rms0));
         } else {
-            if (kt) rms = __dsqrt_rn(__ddiv_rn(kept_sumsq, (double)kt));
-            if (rms == 0.0) st = 1;
+            unsigned long long kt = kept;
+            kt += __shfl_down_sync(0xffffffffu, kept, 1, 4);
+            kt += __shfl_down_sync(0xffffffffu, kept, 2, 4);
+            kt += __shfl_down_sync(0xffffffffu, kept, 3, 4);
+            if (live && k == 0) {
+                uint8_t stt = 0;
+                double rms = rms0;
+                if (n < 2 || rms0 == 0.0) {
+                    stt = 1;
+                } else {
+                    if (kt) rms = __dsqrt_rn(__ddiv_rn(tot, (double)kt));
+                    if (rms == 0.0) stt = 1;
+                }
+                status[row] = stt;
+                frms[row] = __double2float_rn(rms);
+            }
         }
-        status[row] = st;
-        frms[row] = __double2float_rn(rms);
     }
 }
 
@@ -330,65 +366,73 @@ __global__ void __launch_bounds__(BX_THREADS)
                         uint64_t pitch, uint64_t bmax, const double* __restrict__ scale,
                         PeakCtx ctx) {
     constexpr int N = BX_THREADS * S;
-    extern __shared__ double sbuf[];  // [N]
+    // S == 16 (boxcar_max <= 4096): each buffer carries a zero pad of N/4 >= max half so
+    // the shifted read needs no bounds test; S == 24 (8192) tests instead (smem limit).
+    constexpr bool kPad = S == 16;
+    constexpr uint32_t LD = kPad ? N + N / 4 : N;
+    extern __shared__ double sbuf[];  // ping-pong [2][LD]
     const uint32_t row = blockIdx.y;
     if (status[row]) return;
     const uint64_t n = row_len[row];
-    const uint64_t T = N - bmax;
+    const uint32_t T = N - (uint32_t)bmax;
     const uint64_t i0 = (uint64_t)blockIdx.x * T;
     if (i0 >= n) return;
     const float frms = frms_all[row];
-    const size_t base = (size_t)row * pitch;
     const int tid = threadIdx.x;
     const double thr = ctx.cp.threshold;
+    double* cur = sbuf;
+    double* nxt = sbuf + LD;
+    // valid input samples of this tile (32-bit from here on)
+    const uint32_t nin = (uint32_t)(n - i0 < (uint64_t)N ? n - i0 : (uint64_t)N);
+    const size_t base = (size_t)row * pitch + i0;
 
     double r[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) {
-        const uint64_t j = tid + (uint64_t)BX_THREADS * k;
-        const uint64_t i = i0 + j;
+        const uint32_t j = tid + BX_THREADS * k;
         double v = 0.0;
-        if (i < n) v = (double)__fdiv_rn(load_x<KIND>(x_all, base + i), frms);  // :211
+        if (j < nin) v = (double)__fdiv_rn(load_x<KIND>(x_all, base + j), frms);  // :211
         r[k] = v;
-        sbuf[j] = v;
+        cur[j] = v;
     }
+    if (kPad)
+        for (uint32_t j = N + tid; j < LD; j += BX_THREADS) cur[j] = nxt[j] = 0.0;
 
+    // One barrier per level: level l reads `cur` (written at l-1, published by
+    // l-1's __syncthreads_or) and writes `nxt`, which nobody reads until l's barrier.
     uint32_t level = 0;
     for (uint64_t w = 1; w <= bmax && w <= n; w <<= 1, ++level) {
         const uint64_t m = n - w + 1;
         if (w > 1) {
-            const uint64_t half = w >> 1;
-            double sh[S];
-            __syncthreads();
+            const uint32_t half = (uint32_t)(w >> 1);
 #pragma unroll
             for (int k = 0; k < S; ++k) {
-                const uint64_t j = tid + (uint64_t)BX_THREADS * k + half;
-                sh[k] = j < N ? sbuf[j] : 0.0;
+                const uint32_t j = tid + BX_THREADS * k;
+                const double sh = (kPad || j + half < N) ? cur[j + half] : 0.0;
+                r[k] = __dadd_rn(r[k], sh);  // :219
+                nxt[j] = r[k];
             }
-            __syncthreads();
-#pragma unroll
-            for (int k = 0; k < S; ++k) {
-                r[k] = __dadd_rn(r[k], sh[k]);  // :219
-                sbuf[tid + BX_THREADS * k] = r[k];
-            }
+            double* t = cur;
+            cur = nxt;
+            nxt = t;
         }
         const double sc = scale[level];
-        const uint64_t lim2 = m > i0 ? (m - i0 < T ? m - i0 : T) : 0;  // valid local outputs
+        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;  // valid local outputs
         int any = 0;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
-            const uint64_t j = tid + (uint64_t)BX_THREADS * k;
-            any |= (j < lim2) && (__dmul_rn(r[k], sc) > thr);
+            const uint32_t j = tid + BX_THREADS * k;
+            any |= (j < lim2) & (__dmul_rn(r[k], sc) > thr);
         }
         if (__syncthreads_or(any)) {
             // contiguous strip scan: thread owns [tid*S, tid*S + S) of the tile
-            const uint64_t lo = (uint64_t)tid * S;
-            const uint64_t hi = min(lo + S, lim2);
+            const uint32_t lo = (uint32_t)tid * S;
+            const uint32_t hi = min(lo + S, lim2);
             bool in_run = false;
-            uint64_t rb = 0, pk = 0;
+            uint32_t rb = 0, pk = 0;
             double pv = 0.0;
-            for (uint64_t j = lo; j < hi; ++j) {
-                const double v = __dmul_rn(sbuf[j], sc);
+            for (uint32_t j = lo; j < hi; ++j) {
+                const double v = __dmul_rn(cur[j], sc);
                 if (v > thr) {
                     if (!in_run) {
                         in_run = true;
@@ -464,12 +508,15 @@ void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, ui
 void launch_rms(const void* x, int kind, const uint32_t* row_len, uint32_t nrows, uint64_t pitch,
                 float* frms, uint8_t* status, cudaStream_t st) {
     if (!nrows) return;
-    const unsigned threads = 128;
-    const unsigned blocks = (unsigned)((4ull * nrows + threads - 1) / threads);
-    if (kind == 1)
-        rms_kernel<1><<<blocks, threads, 0, st>>>(x, row_len, nrows, pitch, frms, status);
-    else
-        rms_kernel<0><<<blocks, threads, 0, st>>>(x, row_len, nrows, pitch, frms, status);
+    const size_t smem = (size_t)RMS_NST * RMS_TR * RMS_LD * sizeof(float);
+    const unsigned blocks = (nrows + RMS_TR - 1) / RMS_TR;
+    if (kind == 1) {
+        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        rms_kernel<1><<<blocks, 32, smem, st>>>(x, row_len, nrows, pitch, frms, status);
+    } else {
+        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        rms_kernel<0><<<blocks, 32, smem, st>>>(x, row_len, nrows, pitch, frms, status);
+    }
     PGB_CUDA(cudaGetLastError());
 }
 
@@ -482,11 +529,12 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
     if (!nrows || !max_len) return;
     PeakCtx ctx{active, dms, cp, cands, n_cands, cand_cap, frags, n_frags, frag_cap};
     const uint64_t bmax = cp.boxcar_max;
-    const int S = bmax <= 4096 ? 16 : 32;
+    const int S = bmax <= 4096 ? 16 : 24;  // 2 x N doubles must fit in 227 KB
     const uint64_t N = (uint64_t)BX_THREADS * S;
+    const uint64_t LD = S == 16 ? N + N / 4 : N;
     const uint64_t T = N - bmax;
     const unsigned tiles = (unsigned)((max_len + T - 1) / T);
-    const size_t smem = N * sizeof(double);
+    const size_t smem = 2 * LD * sizeof(double);
     dim3 grid(tiles, nrows);
 #define PGB_BX(K, SS)                                                                        \
     do {                                                                                     \
@@ -499,8 +547,8 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
         if (kind == 1) PGB_BX(1, 16);
         else PGB_BX(0, 16);
     } else {
-        if (kind == 1) PGB_BX(1, 32);
-        else PGB_BX(0, 32);
+        if (kind == 1) PGB_BX(1, 24);
+        else PGB_BX(0, 24);
     }
 #undef PGB_BX
     PGB_CUDA(cudaGetLastError());

@@ -31,6 +31,9 @@
 // rounding sequence exactly.
 #include <cuda_pipeline.h>
 
+#include <cstdlib>
+#include <type_traits>
+
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -46,19 +49,25 @@ __device__ __forceinline__ uint32_t warp_max_u32(uint32_t v) {
     return v;
 }
 
-// Per-stage bookkeeping (phase A): for each staged channel slot, the aligned
-// window start and, per trial, the smem byte/element offset of its first sample.
-// Warp w handles channel slot w (G <= DD_WARPS), lane r trial r of the block.
+// Per-stage bookkeeping.  Warp w < G owns channel slot w of a stage and lane r
+// trial r of the block.  The delays of stage g+1 are fetched from global memory
+// one full stage ahead (stage_delay) so their latency hides behind compute; the
+// offsets (window start and per-trial smem offset) are then derived from the
+// register copy (stage_offsets) right before the stage is staged.
+template <int TB>
+__device__ __forceinline__ uint32_t stage_delay(const DedispLaunch& p, uint32_t gi,
+                                                const uint32_t* trial_ids) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t c = gi * p.g + warp;
+    if (warp >= p.g || lane >= TB || c >= p.nchans) return 0;
+    return (uint32_t)__ldg(p.delays_ct + (size_t)c * p.ntrials_plan + trial_ids[lane]);
+}
+
 template <bool U8, int TB>
-__device__ __forceinline__ void stage_offsets(const DedispLaunch& p, uint32_t c0, int b,
-                                              uint64_t i0, const uint32_t* trial_ids,
-                                              uint64_t* abase, uint32_t* offs) {
+__device__ __forceinline__ void stage_offsets(const DedispLaunch& p, uint32_t d, int b,
+                                              uint64_t i0, uint64_t* abase, uint32_t* offs) {
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (warp >= p.g) return;
-    const uint32_t c = c0 + warp;
-    const bool live = c < p.nchans;
-    uint32_t d = 0;
-    if (live && lane < TB) d = (uint32_t)p.delays_ct[(size_t)c * p.ntrials_plan + trial_ids[lane]];
     const uint32_t dmin = warp_min_u32(lane < TB ? d : 0xffffffffu);
     const uint64_t align = U8 ? 16 : 4;  // 16-byte aligned global window start
     const uint64_t a = (i0 + dmin) & ~(align - 1);
@@ -75,7 +84,12 @@ __device__ __forceinline__ void stage_offsets(const DedispLaunch& p, uint32_t c0
 
 constexpr int U8_VPT = 4;  // max 16-byte vectors per thread per stage (host guarantees)
 
-template <int TPW>
+// HMODE selects how the odd samples are accumulated (ablation):
+//   0: H += w >> 8 via __umulhi -> ptxas emits LEA.HI (ALU pipe)
+//   1: H += hi(w * 2^24) via mad.hi (IMAD.HI on the FMA pipe; needs a 64-bit addend pair)
+//   2: S += w as a 64-bit sum via mad.wide (IMAD.WIDE, FMA pipe); decode from S - E
+//   3: as 0, but E accumulates with IMAD (FMA pipe) instead of IADD3 (ALU pipe)
+template <int TPW, int HMODE>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_u8_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
                      int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
@@ -88,10 +102,12 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     uint64_t* abase = reinterpret_cast<uint64_t*>(offs + 2 * G * TB);            // [2][G]
     __shared__ uint32_t trial_ids[32];
 
-    const uint32_t blk = blockIdx.y;
+    // trial blocks vary fastest across the grid so the CTAs in flight share time
+    // tiles of the channel rows through L2
+    const uint32_t blk = blockIdx.x;
     const uint32_t row0 = blk * TB;
     const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
-    const uint64_t i0 = (uint64_t)blockIdx.x * DD_NT;
+    const uint64_t i0 = (uint64_t)blockIdx.y * DD_NT;
     if (i0 >= blk_len[blk]) return;  // every trial of the block is shorter than this tile
     if (threadIdx.x < 32)
         trial_ids[threadIdx.x] = p.active[row0 + min((uint32_t)threadIdx.x, nrows_blk - 1)];
@@ -99,33 +115,36 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nstages = (p.nchans + G - 1) / G;
+    // staging map without divisions: DD_WARPS / G warps per channel slot
+    const int wpc = DD_WARPS / G;
+    const int my_cs = warp / wpc;
+    const uint32_t my_t = (uint32_t)((warp % wpc) * 32 + lane);
+    const uint32_t vstride = (uint32_t)wpc * 32;
     const uint32_t vec_per_ch = W / 16;
-    const uint32_t nvec = (uint32_t)G * vec_per_ch;
+    const uint32_t k24 = p.mul24;  // 1 << 24 from the host: keeps H on the FMA pipe (IMAD.HI)
 
     uint4 v0[U8_VPT];
     uint32_t v1[U8_VPT];
 
     auto load_stage = [&](uint32_t gi, int b) {
-        const uint32_t c0 = gi * G;
+        const uint32_t c = min(gi * G + my_cs, p.nchans - 1);
+        const uint8_t* src = rows + (size_t)c * p.rows_pitch + abase[b * G + my_cs];
 #pragma unroll
         for (int k = 0; k < U8_VPT; ++k) {
-            const uint32_t v = threadIdx.x + k * DD_THREADS;
-            if (v < nvec) {
-                const uint32_t cs = v / vec_per_ch, vi = v - cs * vec_per_ch;
-                const uint32_t c = min(c0 + cs, p.nchans - 1);
-                const uint8_t* src = rows + (size_t)c * p.rows_pitch + abase[b * G + cs] + 16 * vi;
-                v0[k] = __ldg(reinterpret_cast<const uint4*>(src));
-                v1[k] = __ldg(reinterpret_cast<const uint32_t*>(src + 16));
+            const uint32_t vi = my_t + k * vstride;
+            if (vi < vec_per_ch) {
+                v0[k] = __ldg(reinterpret_cast<const uint4*>(src + 16 * vi));
+                v1[k] = __ldg(reinterpret_cast<const uint32_t*>(src + 16 * vi + 16));
             }
         }
     };
     auto store_stage = [&](int b) {
+        uint8_t* base = buf + (size_t)((b * G + my_cs) * 4) * W;
 #pragma unroll
         for (int k = 0; k < U8_VPT; ++k) {
-            const uint32_t v = threadIdx.x + k * DD_THREADS;
-            if (v < nvec) {
-                const uint32_t cs = v / vec_per_ch, vi = v - cs * vec_per_ch;
-                uint8_t* dst = buf + (size_t)((b * G + cs) * 4) * W + 16 * vi;
+            const uint32_t vi = my_t + k * vstride;
+            if (vi < vec_per_ch) {
+                uint8_t* dst = base + 16 * vi;
                 const uint32_t w[5] = {v0[k].x, v0[k].y, v0[k].z, v0[k].w, v1[k]};
                 *reinterpret_cast<uint4*>(dst) = v0[k];
 #pragma unroll
@@ -142,7 +161,10 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
         }
     };
 
-    uint32_t E[TPW][DD_WORDS], H[TPW][DD_WORDS];
+    using HT = typename std::conditional<HMODE == 2, unsigned long long, uint32_t>::type;
+    uint32_t E[TPW][DD_WORDS];
+    HT H[TPW][DD_WORDS];
+    const uint32_t one = p.mul24 >> 24;  // 1, opaque to the compiler
 #pragma unroll
     for (int u = 0; u < TPW; ++u)
 #pragma unroll
@@ -158,9 +180,15 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 #pragma unroll
                 for (int m = 0; m < DD_WORDS; ++m) {
                     const uint32_t q = lane + 32 * m;
-                    const uint32_t e = E[u][m], h = H[u][m];
+                    const uint32_t e = E[u][m];
                     const uint32_t b0 = e & 0xffffu, b2 = e >> 16;
-                    const uint32_t t = h - (b2 << 8);
+                    uint32_t t;
+                    if (HMODE == 2) {
+                        const unsigned long long d = H[u][m] - e;  // 2^8 B1 + 2^24 B3
+                        t = (uint32_t)((d >> 8) & 0xffffu) | (uint32_t)(d >> 24) << 16;
+                    } else {
+                        t = (uint32_t)H[u][m] - (b2 << 8);  // B1 + 2^16 B3
+                    }
                     int4 val = make_int4((int)b0, (int)(t & 0xffffu), (int)b2, (int)(t >> 16));
                     int4* pd = reinterpret_cast<int4*>(dst + 4 * q);
                     if (!first_flush) {
@@ -179,8 +207,10 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
         first_flush = false;
     };
 
-    // prologue: stage 0
-    stage_offsets<true, TB>(p, 0, 0, i0, trial_ids, abase, offs);
+    // prologue: stage 0 offsets and data; delays of stage 1 in flight
+    uint32_t dnext = stage_delay<TB>(p, 0, trial_ids);
+    stage_offsets<true, TB>(p, dnext, 0, i0, abase, offs);
+    dnext = nstages > 1 ? stage_delay<TB>(p, 1, trial_ids) : 0;
     __syncthreads();
     load_stage(0, 0);
     store_stage(0);
@@ -189,7 +219,10 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     for (uint32_t gi = 0; gi < nstages; ++gi) {
         const int b = gi & 1;
         const bool more = gi + 1 < nstages;
-        if (more) stage_offsets<true, TB>(p, (gi + 1) * G, b ^ 1, i0, trial_ids, abase, offs);
+        if (more) {
+            stage_offsets<true, TB>(p, dnext, b ^ 1, i0, abase, offs);
+            if (gi + 2 < nstages) dnext = stage_delay<TB>(p, gi + 2, trial_ids);
+        }
         __syncthreads();
         if (more) load_stage(gi + 1, b ^ 1);
 
@@ -204,8 +237,24 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 #pragma unroll
                 for (int m = 0; m < DD_WORDS; ++m) {
                     const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 128 * m);
-                    E[u][m] += w & 0x00ff00ffu;
-                    H[u][m] = __umulhi(w, 1u << 24) + H[u][m];
+                    if (HMODE == 3) {  // E on the FMA pipe (IMAD), H on the ALU pipe (LEA.HI)
+                        uint32_t e = E[u][m];
+                        asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(e) : "r"(w & 0x00ff00ffu), "r"(one));
+                        E[u][m] = e;
+                    } else {
+                        E[u][m] += w & 0x00ff00ffu;  // samples 0 and 2 (LOP3 + IADD3, ALU pipe)
+                    }
+                    if (HMODE == 0 || HMODE == 3) {
+                        H[u][m] += __umulhi(w, 1u << 24);
+                    } else if (HMODE == 1) {
+                        uint32_t h = (uint32_t)H[u][m];
+                        asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(w), "r"(k24));
+                        H[u][m] = h;
+                    } else {
+                        unsigned long long h = H[u][m];
+                        asm("mad.wide.u32 %0, %1, %2, %0;" : "+l"(h) : "r"(w), "r"(one));
+                        H[u][m] = h;
+                    }
                 }
             }
         }
@@ -228,10 +277,10 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     uint64_t* abase = reinterpret_cast<uint64_t*>(offs + 2 * G * TB);
     __shared__ uint32_t trial_ids[32];
 
-    const uint32_t blk = blockIdx.y;
+    const uint32_t blk = blockIdx.x;
     const uint32_t row0 = blk * TB;
     const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
-    const uint64_t i0 = (uint64_t)blockIdx.x * DD_NT;
+    const uint64_t i0 = (uint64_t)blockIdx.y * DD_NT;
     if (i0 >= blk_len[blk]) return;
     if (threadIdx.x < 32)
         trial_ids[threadIdx.x] = p.active[row0 + min((uint32_t)threadIdx.x, nrows_blk - 1)];
@@ -239,17 +288,18 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nstages = (p.nchans + G - 1) / G;
+    const int wpc = DD_WARPS / G;
+    const int my_cs = warp / wpc;
+    const uint32_t my_t = (uint32_t)((warp % wpc) * 32 + lane);
+    const uint32_t vstride = (uint32_t)wpc * 32;
     const uint32_t vec_per_ch = W / 4;
-    const uint32_t nvec = (uint32_t)G * vec_per_ch;
 
     auto issue_stage = [&](uint32_t gi, int b) {
-        const uint32_t c0 = gi * G;
-        for (uint32_t v = threadIdx.x; v < nvec; v += DD_THREADS) {
-            const uint32_t cs = v / vec_per_ch, vi = v - cs * vec_per_ch;
-            const uint32_t c = min(c0 + cs, p.nchans - 1);
-            const float* src = rows + (size_t)c * p.rows_pitch + abase[b * G + cs] + 4 * vi;
-            __pipeline_memcpy_async(buf + (size_t)(b * G + cs) * W + 4 * vi, src, 16);
-        }
+        const uint32_t c = min(gi * G + my_cs, p.nchans - 1);
+        const float* src = rows + (size_t)c * p.rows_pitch + abase[b * G + my_cs];
+        float* dst = buf + (size_t)(b * G + my_cs) * W;
+        for (uint32_t vi = my_t; vi < vec_per_ch; vi += vstride)
+            __pipeline_memcpy_async(dst + 4 * vi, src + 4 * vi, 16);
         __pipeline_commit();
     };
 
@@ -259,14 +309,19 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 #pragma unroll
         for (int m = 0; m < DD_FOUT; ++m) acc[u][m] = 0.0f;  // the reference starts from +0.0f
 
-    stage_offsets<false, TB>(p, 0, 0, i0, trial_ids, abase, offs);
+    uint32_t dnext = stage_delay<TB>(p, 0, trial_ids);
+    stage_offsets<false, TB>(p, dnext, 0, i0, abase, offs);
+    dnext = nstages > 1 ? stage_delay<TB>(p, 1, trial_ids) : 0;
     __syncthreads();
     issue_stage(0, 0);
 
     for (uint32_t gi = 0; gi < nstages; ++gi) {
         const int b = gi & 1;
         const bool more = gi + 1 < nstages;
-        if (more) stage_offsets<false, TB>(p, (gi + 1) * G, b ^ 1, i0, trial_ids, abase, offs);
+        if (more) {
+            stage_offsets<false, TB>(p, dnext, b ^ 1, i0, abase, offs);
+            if (gi + 2 < nstages) dnext = stage_delay<TB>(p, gi + 2, trial_ids);
+        }
         __pipeline_wait_prior(0);
         __syncthreads();
         if (more) issue_stage(gi + 1, b ^ 1);
@@ -360,23 +415,33 @@ size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax) {
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
     const size_t smem = dedisp_smem_bytes(true, p.g, p.wmax);
     const int tb = DD_WARPS * p.tpw;
-    dim3 grid(p.ntiles, (p.nrows + tb - 1) / tb);
+    dim3 grid((p.nrows + tb - 1) / tb, p.ntiles);
+    static const int mode = [] {
+        const char* e = getenv("PGB_DD_HMODE");
+        return e ? atoi(e) : 3;
+    }();
+#define PGB_DD(TPW, M)                                                                          \
+    do {                                                                                        \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_kernel<TPW, M>,                                 \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
+        dedisp_u8_kernel<TPW, M><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);      \
+    } while (0)
     if (p.tpw == 2) {
-        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_kernel<2>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dedisp_u8_kernel<2><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);
+        if (mode == 1) PGB_DD(2, 1);
+        else if (mode == 3) PGB_DD(2, 3);
+        else if (mode == 2) PGB_DD(2, 2);
+        else PGB_DD(2, 0);
     } else {
-        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_kernel<1>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        dedisp_u8_kernel<1><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);
+        PGB_DD(1, 0);
     }
+#undef PGB_DD
     PGB_CUDA(cudaGetLastError());
 }
 
 void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st) {
     const size_t smem = dedisp_smem_bytes(false, p.g, p.wmax);
     const int tb = DD_WARPS * p.tpw;
-    dim3 grid(p.ntiles, (p.nrows + tb - 1) / tb);
+    dim3 grid((p.nrows + tb - 1) / tb, p.ntiles);
     if (p.tpw == 2) {
         PGB_CUDA(cudaFuncSetAttribute(dedisp_f32_kernel<2>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

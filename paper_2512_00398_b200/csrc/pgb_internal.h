@@ -101,7 +101,8 @@ struct DedispLaunch {
     int tpw;                    // trials per warp (2 -> 32-trial blocks, 1 -> 16)
     int g;                      // channels per stage
     uint32_t wmax;              // staged window length (elements)
-    uint32_t ntiles;            // time tiles (grid.x)
+    uint32_t ntiles;            // time tiles (grid.y)
+    uint32_t mul24;             // 1 << 24, passed at run time (see dedisp_u8_kernel)
 };
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st);
 void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st);

@@ -306,16 +306,19 @@ class Engine:
 
     # ---- file-level search ------------------------------------------------------------
     def search_file(self, payload, nsamples: int, chunks: list[ChunkSpec], plan: DmTrialPlan,
-                    cfg: EngineConfig, *, trial_range: tuple[int, int] | None = None):
+                    cfg: EngineConfig, *, trial_range: tuple[int, int] | None = None,
+                    cluster: bool = True):
         """execute_task's chunk loop + sort + link_grid on a raw 8-bit payload.
 
-        Returns (candidates, clusters, skipped (chunk, trial) pairs)."""
+        Returns (candidates, clusters, skipped (chunk, trial) pairs).  cluster=False
+        stops after the sorted candidates (multi-GPU shards cluster after the gather)."""
         self.set_plan(plan, trial_range)
         arr = np.zeros(len(chunks), abi.CHUNK_SPEC_DTYPE)
         for k, c in enumerate(chunks):
             arr[k] = (c.index, c.start_sample, c.length, c.overlap, c.valid_begin, c.valid_end)
         ccfg = cfg._c()
         r = cfg.radii._c()
+        rp = ctypes.byref(r) if cluster else None
         nc, ncl = ctypes.c_size_t(), ctypes.c_size_t()
         dev = _device_tensor(payload)
         if dev is not None:
@@ -327,8 +330,7 @@ class Engine:
             payload = np.ascontiguousarray(payload, dtype=np.uint8)
             ptr, on_dev = abi.ptr(payload), 0
         check(lib.pgb_search_file_u8(self._h, ptr, on_dev, int(nsamples), abi.ptr(arr), len(arr),
-                                     ctypes.byref(ccfg), ctypes.byref(r), ctypes.byref(nc),
-                                     ctypes.byref(ncl)))
+                                     ctypes.byref(ccfg), rp, ctypes.byref(nc), ctypes.byref(ncl)))
         return self.fetch_file_results(nc.value, ncl.value)
 
     def fetch_file_results(self, nc: int, ncl: int):
