@@ -74,11 +74,15 @@ def gather_candidates(local: np.ndarray, *, device=None, group=None) -> np.ndarr
     dist.all_gather(bufs, buf, group=group)
     if rank != 0:
         return None
-    parts = []
+    # (np.concatenate would canonicalise the padded 72-byte record dtype)
+    merged = np.zeros(sum(counts), abi.CANDIDATE_DTYPE)
+    raw = merged.view(np.uint8)
+    off = 0
     for r, b in enumerate(bufs):
         if counts[r]:
-            parts.append(b[: counts[r] * itemsize].cpu().numpy().view(abi.CANDIDATE_DTYPE))
-    merged = np.concatenate(parts) if parts else np.zeros(0, abi.CANDIDATE_DTYPE)
+            nb = counts[r] * itemsize
+            raw[off: off + nb] = b[:nb].cpu().numpy()
+            off += nb
     return sort_candidates(merged)
 
 
