@@ -40,6 +40,8 @@ def build(native: bool = False) -> None:
     subprocess.run(["make", "-s", "-C", str(HERE), "oracle"], check=True)
     if Path("/root/reference/proj/src").is_dir():
         subprocess.run(["make", "-s", "-C", str(HERE), "ref"], check=True)
+        if (HERE.parent / "paper_2512_00398_b200" / "libpgb200.so").exists():
+            subprocess.run(["make", "-s", "-C", str(HERE), "dropin"], check=True)
         if native:
             subprocess.run(["make", "-s", "-C", str(HERE), "native"], check=True)
 

@@ -113,7 +113,7 @@ struct pgb_context {
     // device work buffers
     DevBuf in_raw, rows, series, base, frms, status, d_active, d_row_len, d_blk_len, d_scale;
     DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
-    DevBuf payload;
+    DevBuf payload, in_u8;
     DevBuf file_cands, file_sorted;
     DevBuf cl_scratch, clusters, members;
     PinnedBuf h_counters;
@@ -531,7 +531,7 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         cudaStreamSynchronize(ctx->copy_st);
         for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,
                           &ctx->base, &ctx->frms, &ctx->status, &ctx->d_active, &ctx->d_row_len,
-                          &ctx->d_blk_len, &ctx->d_scale, &ctx->cands_raw, &ctx->cands_sorted,
+                          &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->cands_raw, &ctx->cands_sorted,
                           &ctx->frags, &ctx->frags_sorted, &ctx->counters, &ctx->sort_keys,
                           &ctx->sort_idx, &ctx->sort_tmp, &ctx->payload, &ctx->file_cands,
                           &ctx->file_sorted, &ctx->cl_scratch, &ctx->clusters, &ctx->members})
@@ -609,7 +609,29 @@ static pgb_status run_dm_loop_impl(pgb_context* ctx, const void* data, bool u8, 
             PGB_CUDA(cudaMemcpyAsync(ctx->in_raw.p, data, bytes, cudaMemcpyHostToDevice, ctx->st));
             dptr = ctx->in_raw.p;
         }
-        run_chunk(ctx, ChunkInput{dptr, u8}, spec, cfg);
+        bool as_u8 = u8;
+        if (!u8 && ctx->ntrials && spec->length && !getenv("PGB_FORCE_F32_PATH")) {
+            // Widened 8-bit chunks (read_chunk, src/filterbank.cpp:304-307) hold integers in
+            // [0, 255]: every in-order fp32 partial sum is then an exact integer, so the
+            // integer path gives bit-identical series and baselines.  Repack on the device.
+            const size_t cells = (size_t)spec->length * ctx->nchans;
+            ctx->in_u8.reserve(cells);
+            ctx->counters.reserve(4 * sizeof(unsigned long long));
+            ctx->h_counters.reserve(4 * sizeof(unsigned long long));
+            auto* dflag = ctx->counters.as<unsigned long long>() + 2;
+            PGB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(unsigned long long), ctx->st));
+            launch_pack_u8(static_cast<const float*>(dptr), cells, ctx->in_u8.as<uint8_t>(), dflag,
+                           ctx->st);
+            auto* hflag = ctx->h_counters.as<unsigned long long>() + 2;
+            PGB_CUDA(cudaMemcpyAsync(hflag, dflag, sizeof *hflag, cudaMemcpyDeviceToHost, ctx->st));
+            PGB_CUDA(cudaStreamSynchronize(ctx->st));
+            ctx->launches += 1;
+            if (*hflag == 0) {
+                dptr = ctx->in_u8.p;
+                as_u8 = true;
+            }
+        }
+        run_chunk(ctx, ChunkInput{dptr, as_u8}, spec, cfg);
         if (n_candidates) *n_candidates = ctx->n_cands;
         if (n_skipped) *n_skipped = ctx->skipped.size();
     });

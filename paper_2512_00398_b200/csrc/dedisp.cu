@@ -404,7 +404,40 @@ __global__ void transpose_f32_kernel(const float* __restrict__ in, uint64_t leng
     }
 }
 
+__global__ void pack_u8_kernel(const float* __restrict__ in, size_t cells, uint8_t* __restrict__ out,
+                               unsigned long long* not_u8) {
+    const size_t n4 = cells / 4;
+    bool bad = false;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (size_t)gridDim.x * blockDim.x) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(in) + i);
+        const float f[4] = {v.x, v.y, v.z, v.w};
+        uint32_t w = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const bool ok = f[k] >= 0.0f && f[k] <= 255.0f && f[k] == truncf(f[k]);
+            bad |= !ok;
+            w |= (ok ? (uint32_t)f[k] : 0u) << (8 * k);
+        }
+        reinterpret_cast<uint32_t*>(out)[i] = w;
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0)
+        for (size_t i = 4 * n4; i < cells; ++i) {
+            const float f = in[i];
+            const bool ok = f >= 0.0f && f <= 255.0f && f == truncf(f);
+            bad |= !ok;
+            out[i] = ok ? (uint8_t)f : 0;
+        }
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(not_u8, 1ull);
+}
+
 }  // namespace
+
+void launch_pack_u8(const float* in, size_t cells, uint8_t* out, unsigned long long* not_u8,
+                    cudaStream_t st) {
+    pack_u8_kernel<<<148 * 8, 256, 0, st>>>(in, cells, out, not_u8);
+    PGB_CUDA(cudaGetLastError());
+}
 
 size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax) {
     const int tb = 32;

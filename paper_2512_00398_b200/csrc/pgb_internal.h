@@ -85,6 +85,9 @@ struct ChainParams {
 // u8 [length][nchans] -> rows [nchans][pitch]
 void launch_transpose_u8(const uint8_t* in, uint64_t length, uint32_t nchans, uint8_t* rows,
                          uint64_t pitch, cudaStream_t st);
+// f32 cells -> u8 codes; sets *not_u8 to 1 if any cell is not an integer in [0, 255]
+void launch_pack_u8(const float* in, size_t cells, uint8_t* out, unsigned long long* not_u8,
+                    cudaStream_t st);
 void launch_transpose_f32(const float* in, uint64_t length, uint32_t nchans, float* rows,
                           uint64_t pitch, cudaStream_t st);
 

@@ -137,6 +137,21 @@ def test_run_dm_loop_f32_engine_workload(engine, ref):
     assert abs(best["dm"] - 100.0) <= 2.0 and abs(int(best["peak_sample"]) - 2000) <= 4
 
 
+def test_widened_u8_chunk_takes_integer_path(engine, port, monkeypatch):
+    """A float chunk of 8-bit codes (read_chunk's widening) is repacked on the device;
+    results equal the u8 path, the forced fp32 path and the oracle."""
+    hdr, plan, data = _small_u8_case()
+    cfg = EngineConfig(n_workers=2, tsamp=hdr.tsamp, boxcar_max=256, baseline_window=2001)
+    spec = ChunkSpec.whole(data.shape[0])
+    a = engine.run_dm_loop(Chunk(spec, data), plan, cfg)
+    b = engine.run_dm_loop(Chunk(spec, data.astype(np.float32)), plan, cfg)
+    monkeypatch.setenv("PGB_FORCE_F32_PATH", "1")
+    c = engine.run_dm_loop(Chunk(spec, data.astype(np.float32)), plan, cfg)
+    want, _ = port.run_dm_loop(data, vars(spec), plan.dms, plan.delays, cfg_dict(cfg))
+    for r in (a, b, c):
+        assert_same_candidates(r.candidates, want)
+
+
 def test_snr_within_stated_tolerance(engine, ref):
     hdr, plan, g = _float_workload(ref)
     cfg = EngineConfig(n_workers=2, tsamp=hdr.tsamp, boxcar_max=64, baseline_window=1001)
