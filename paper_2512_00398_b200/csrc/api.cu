@@ -113,7 +113,7 @@ struct pgb_context {
     // device work buffers
     DevBuf in_raw, rows, series, base, frms, status, d_active, d_row_len, d_blk_len, d_scale;
     DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
-    DevBuf payload, in_u8;
+    DevBuf payload, in_u8, ws_base, ws_off;
     DevBuf file_cands, file_sorted;
     DevBuf cl_scratch, clusters, members;
     PinnedBuf h_counters;
@@ -261,9 +261,29 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     if (dedisp_smem_bytes(u8, g, wmax) > DD_SMEM_BUDGET || (u8 && (uint64_t)g * wmax / 16 > 4ull * DD_THREADS))
         raise(PGB_ERR_CONFIG, "per-block channel delay spread of " + std::to_string(spread) +
                                   " samples exceeds the dedispersion staging capacity");
+    // warp-specialized TMA kernel (u8): 16-byte aligned window starts, 256-byte boxes,
+    // >= 20 bytes of slack for the packers' funnel shifts; deepest ring that fits
+    int ws_g = 0, ws_ns = 0;
+    const uint32_t ws_wmax = (uint32_t)round_up(spread + DD_NT + 16 + 20, 2048);
+    if (u8 && dedisp_ws_available()) {
+        const int cand[][2] = {{8, 4}, {8, 3}, {4, 4}, {4, 3}, {8, 2}, {2, 4}, {4, 2}, {2, 3}, {1, 4}, {1, 2}};
+        for (const auto& c : cand)
+            if (dedisp_ws_smem_bytes(c[0], ws_wmax, c[1]) <= 220 * 1024) {
+                ws_g = c[0];
+                ws_ns = c[1];
+                break;
+            }
+        const char* eg = getenv("PGB_WS_G");  // geometry overrides (experiments)
+        const char* en = getenv("PGB_WS_NS");
+        if (eg && en && dedisp_ws_smem_bytes(atoi(eg), ws_wmax, atoi(en)) <= 220 * 1024) {
+            ws_g = atoi(eg);
+            ws_ns = atoi(en);
+        }
+    }
     const uint32_t ntiles = (uint32_t)((max_n + DD_NT - 1) / DD_NT);
     const uint64_t out_pitch = (uint64_t)ntiles * DD_NT;
-    const uint64_t rows_pitch = round_up((uint64_t)ntiles * DD_NT + maxd_active + wmax + 64, 64);
+    const uint64_t rows_pitch =
+        round_up((uint64_t)ntiles * DD_NT + maxd_active + std::max(wmax, ws_wmax) + 64, 64);
     const size_t esz = u8 ? 1 : 4;
 
     ctx->rows.reserve((size_t)C * rows_pitch * esz, true);
@@ -310,7 +330,20 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     dl.ntiles = ntiles;
     dl.mul24 = 1u << 24;
     PGB_CUDA(cudaEventRecord(ctx->ev_dd0, st));
-    if (u8) launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+    if (u8 && ws_g) {
+        DedispLaunch dw = dl;
+        dw.g = ws_g;
+        dw.wmax = ws_wmax;
+        dw.nchans_pad = (C + 7) & ~7u;
+        ctx->ws_base.reserve((size_t)nblocks * C * 4);
+        ctx->ws_off.reserve((size_t)nblocks * dw.nchans_pad * 32 * 2);
+        dw.wbase = ctx->ws_base.as<uint32_t>();
+        dw.woff = ctx->ws_off.as<uint16_t>();
+        launch_ws_offsets(dw, ctx->ws_base.as<uint32_t>(), ctx->ws_off.as<uint16_t>(), st);
+        ctx->launches += 1;
+        launch_dedisp_u8_ws(dw, ws_ns, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+    } else if (u8)
+        launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
     else launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
     PGB_CUDA(cudaEventRecord(ctx->ev_dd1, st));
     ctx->dedisp_launches += 1;
@@ -531,7 +564,7 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         cudaStreamSynchronize(ctx->copy_st);
         for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,
                           &ctx->base, &ctx->frms, &ctx->status, &ctx->d_active, &ctx->d_row_len,
-                          &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->cands_raw, &ctx->cands_sorted,
+                          &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->ws_base, &ctx->ws_off, &ctx->cands_raw, &ctx->cands_sorted,
                           &ctx->frags, &ctx->frags_sorted, &ctx->counters, &ctx->sort_keys,
                           &ctx->sort_idx, &ctx->sort_tmp, &ctx->payload, &ctx->file_cands,
                           &ctx->file_sorted, &ctx->cl_scratch, &ctx->clusters, &ctx->members})

@@ -106,10 +106,20 @@ struct DedispLaunch {
     uint32_t wmax;              // staged window length (elements)
     uint32_t ntiles;            // time tiles (grid.y)
     uint32_t mul24;             // 1 << 24, passed at run time (see dedisp_u8_kernel)
+    // warp-specialized kernel only: tile-independent window bases / trial offsets
+    const uint32_t* wbase;      // [nblocks][nchans] 16-byte aligned minimum delay
+    const uint16_t* woff;       // [nblocks][nchans_pad][32] delay - wbase
+    uint32_t nchans_pad;        // nchans rounded up to 8
 };
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st);
 void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st);
 size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax);
+// warp-specialized TMA variant (dedisp_tma.cu); p.wmax (bytes) must be a multiple of 256
+void launch_dedisp_u8_ws(const DedispLaunch& p, int nslot, const uint8_t* rows, int32_t* out,
+                         cudaStream_t st);
+size_t dedisp_ws_smem_bytes(int g, uint32_t wmax, int nslot);
+void launch_ws_offsets(const DedispLaunch& p, uint32_t* wbase, uint16_t* woff, cudaStream_t st);
+bool dedisp_ws_available();
 
 // chain
 void launch_baseline_int(const int32_t* x, float* out, const uint32_t* row_len, uint32_t nrows,
