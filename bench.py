@@ -110,7 +110,7 @@ def make_payload(cfg, plan, rows: int | None = None, device: str = "cuda"):
 
 def build_task(cfg):
     from paper_2512_00398_b200.dedisp import FilterbankHeader, LinearSpacing
-    from paper_2512_00398_b200.engine import EngineConfig
+    from paper_2512_00398_b200.engine import EngineConfig, RfiConfig
     from paper_2512_00398_b200.pipeline import SearchParams, create_task
 
     hdr = FilterbankHeader(fch1=cfg["fch1"], foff=cfg["foff"], nchans=cfg["nchans"],
@@ -118,7 +118,8 @@ def build_task(cfg):
     params = SearchParams(dm_lo=cfg["dm_lo"], dm_hi=cfg["dm_hi"], spacing=LinearSpacing(cfg["dm_step"]),
                           engine=EngineConfig(n_workers=1, detect_thresh=cfg["detect_thresh"],
                                               boxcar_max=cfg["boxcar_max"]),
-                          baseline_len_s=cfg["baseline_s"], nsamps_chunk=cfg["nsamps_chunk"])
+                          baseline_len_s=cfg["baseline_s"], nsamps_chunk=cfg["nsamps_chunk"],
+                          rfi=RfiConfig(narrowband=cfg.get("rfi", False), broadband=cfg.get("rfi", False)))
     return create_task(hdr, params)
 
 
@@ -204,7 +205,7 @@ def run_reference_arm(args, cfg, rank: int):
     plan = task.plan
     threads = os.cpu_count() or 1
     chunk0 = make_payload(cfg, plan, rows=task.chunks[0].length, device="cpu").numpy()
-    per_step = float(os.environ.get("PG_REF_STEP_S", "3.0"))
+    per_step = float(os.environ.get("PG_REF_STEP_S", "8.0"))
     for _ in range(args.warmup):
         reference_sample(cfg, plan, task, chunk0, per_step, threads)
     rates, walls, desc = [], [], ""

@@ -45,6 +45,7 @@ typedef enum pgb_status {
     PGB_ERR_DEGENERATE = 5,      /* pulsegrid::degenerate_series_error errors.hpp:44-46 */
     PGB_ERR_INVALID_PLAN = 6,    /* pulsegrid::invalid_plan_error      errors.hpp:24-26 */
     PGB_ERR_ARGUMENT = 7,        /* bad pointer / size (std::invalid_argument) */
+    PGB_ERR_INSUFFICIENT = 8,    /* pulsegrid::insufficient_statistics_error errors.hpp:40-42 */
     PGB_ERR_NO_DEVICE = 100,     /* no sm_100 device visible */
     PGB_ERR_CUDA = 101,          /* CUDA runtime / kernel failure */
     PGB_ERR_OOM = 102            /* device allocation failed */
@@ -119,6 +120,16 @@ typedef struct pgb_header {
 } pgb_header;
 
 typedef enum pgb_spacing { PGB_SPACING_LINEAR = 0, PGB_SPACING_ADAPTIVE = 1 } pgb_spacing;
+
+/* RFI excision settings (SearchParams, pipeline.hpp:31-35; rfi.hpp:10-33). */
+typedef struct pgb_rfi_config {
+    int32_t narrowband;  /* flag_narrowband (src/rfi.cpp:32-68) */
+    int32_t broadband;   /* flag_broadband (src/rfi.cpp:70-91) */
+    double k_sigma;
+    double k_mad;
+    int32_t local_mean;  /* MaskPolicy::local_mean (1) or zero (0), src/rfi.cpp:93-139 */
+    int32_t _pad;
+} pgb_rfi_config;
 
 typedef struct pgb_context pgb_context;
 
@@ -195,7 +206,18 @@ pgb_status pgb_fetch_clusters(pgb_context* ctx, pgb_cluster* out, size_t capacit
 pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payload_on_device,
                               uint64_t nsamples, const pgb_chunk_spec* chunks, size_t nchunks,
                               const pgb_engine_config* cfg, const pgb_link_radii* radii,
-                              size_t* n_candidates, size_t* n_clusters);
+                              const pgb_rfi_config* rfi, size_t* n_candidates,
+                              size_t* n_clusters);
+
+/* ---- RFI excision (next row f1: the reference runs it before run_dm_loop) ------- */
+/* Flags (narrowband channels, broadband samples) and masks one time-major chunk
+ * [length][nchans] (u8 codes or floats; host or device) into a float chunk, exactly
+ * as flag_narrowband + flag_broadband + apply_mask do.  out_host (optional) receives
+ * the cleaned chunk; the flags stay fetchable with pgb_fetch_rfi_flags. */
+pgb_status pgb_rfi_clean(pgb_context* ctx, const void* data, int is_u8, int on_device,
+                         uint64_t length, const pgb_rfi_config* rfi, float* out_host,
+                         uint64_t* n_bad_channels, uint64_t* n_bad_samples);
+pgb_status pgb_fetch_rfi_flags(pgb_context* ctx, uint8_t* bad_channels, uint8_t* bad_samples);
 pgb_status pgb_fetch_file_candidates(pgb_context* ctx, pgb_candidate* out, size_t capacity);
 /* (chunk index, trial) pairs, as FileOutcome::skipped_trials (pipeline.hpp:59). */
 pgb_status pgb_fetch_file_skipped(pgb_context* ctx, uint64_t* chunk_trial_pairs,

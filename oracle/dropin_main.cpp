@@ -9,7 +9,7 @@
 // on the same SIGPROC file and write the reference's .cand text; the test compares
 // the files byte for byte.
 //
-// usage: pipeline_* in.fil out.cand dm_lo dm_hi dm_step boxcar_max baseline_s nsamps_chunk n_workers
+// usage: pipeline_* in.fil out.cand dm_lo dm_hi dm_step boxcar_max baseline_s nsamps_chunk n_workers [rfi]
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -18,7 +18,7 @@
 
 int main(int argc, char** argv) {
     using namespace pulsegrid;
-    if (argc != 10) {
+    if (argc != 10 && argc != 11) {
         std::fprintf(stderr, "usage: %s in.fil out.cand dm_lo dm_hi dm_step boxcar baseline_s chunk workers\n",
                      argv[0]);
         return 2;
@@ -33,8 +33,9 @@ int main(int argc, char** argv) {
         p.nsamps_chunk = std::strtoull(argv[8], nullptr, 10);
         p.engine.n_workers = (std::uint32_t)std::atoi(argv[9]);
         p.engine.max_in_flight = p.engine.n_workers;  // parity mode (block size 1)
-        p.rfi_narrowband = false;
-        p.rfi_broadband = false;
+        const bool rfi = argc == 11 && std::atoi(argv[10]) != 0;  // reference defaults when on
+        p.rfi_narrowband = rfi;
+        p.rfi_broadband = rfi;
         auto task = create_task(argv[1], p, argv[2]);
         BufferPool pool(p.engine.memory_budget);
         auto out = execute_task(task, pool);

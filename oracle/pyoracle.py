@@ -271,6 +271,19 @@ class Reference(_Base):
         h = _header(fch1, foff, tsamp, grid.shape[1])
         self._check(f(abi.ptr(grid), grid.shape[0], _c.byref(h), dm, t0, width, amplitude))
 
+    def rfi(self, data: np.ndarray, *, narrowband=True, broadband=True, k_sigma=6.0, k_mad=5.0,
+            local_mean=True):
+        """(cleaned float chunk, bad-channel mask, bad-sample mask) of the reference RFI stage."""
+        x = np.ascontiguousarray(data, np.float32).copy()
+        L, nch = x.shape
+        bc = np.zeros(nch, np.uint8)
+        bs = np.zeros(L, np.uint8)
+        f = self._fn("rfi", [_vp, _u64, _u32, _c.c_int, _c.c_int, _c.c_double, _c.c_double, _c.c_int,
+                             _vp, _vp])
+        self._check(f(abi.ptr(x), L, nch, int(narrowband), int(broadband), k_sigma, k_mad,
+                      int(local_mean), abi.ptr(bc), abi.ptr(bs)))
+        return x, bc.astype(bool), bs.astype(bool)
+
     def amplitude_for_snr(self, snr, sigma, nchans, width) -> float:
         f = self._fn("amplitude_for_snr", [_c.c_double, _c.c_double, _u32, _u64], _c.c_double)
         return float(f(snr, sigma, nchans, width))

@@ -28,6 +28,7 @@
 #include "pulsegrid/engine.hpp"
 #include "pulsegrid/filterbank.hpp"
 #include "pulsegrid/pipeline.hpp"
+#include "pulsegrid/rfi.hpp"
 #include "pulsegrid/synth.hpp"
 
 using namespace pulsegrid;
@@ -397,6 +398,36 @@ int pgref_write_filterbank(const char* path, const pgb_header* h, uint32_t nbits
         std::ofstream out(path, std::ios::binary);
         write_filterbank(fh, std::span<const float>(samples, nsamples * h->nchans), out);
         return out ? PGB_OK : PGB_ERR_ARGUMENT;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// flag_narrowband + flag_broadband + apply_mask on one widened chunk
+// (src/rfi.cpp:32-139; execute_task's order, src/pipeline.cpp:79-87).  `data` is
+// cleaned in place; bad channel / sample masks are returned as 0/1 bytes.
+int pgref_rfi(float* data, uint64_t length, uint32_t nchans, int narrowband, int broadband,
+              double k_sigma, double k_mad, int local_mean, uint8_t* bad_ch, uint8_t* bad_s) {
+    try {
+        Chunk chunk;
+        chunk.spec.length = length;
+        chunk.spec.valid_end = length;
+        chunk.nchans = nchans;
+        chunk.data.assign(data, data + length * nchans);
+        RfiMask mask;
+        mask.replacement = local_mean ? MaskPolicy::local_mean : MaskPolicy::zero;
+        if (narrowband) mask.bad_channels = flag_narrowband(chunk, k_mad);
+        if (broadband) mask.bad_samples = flag_broadband(chunk, k_sigma);
+        if (!mask.bad_channels.empty() || !mask.bad_samples.empty()) apply_mask(chunk, mask);
+        std::memcpy(data, chunk.data.data(), length * nchans * sizeof(float));
+        std::memset(bad_ch, 0, nchans);
+        std::memset(bad_s, 0, length);
+        for (auto c : mask.bad_channels) bad_ch[c] = 1;
+        for (auto s : mask.bad_samples) bad_s[s] = 1;
+        return PGB_OK;
+    } catch (const insufficient_statistics_error& e) {
+        g_err = e.what();
+        return PGB_ERR_INSUFFICIENT;
     } catch (const std::exception& e) {
         return fail(e);
     }

@@ -51,7 +51,9 @@ SIGNATURES = {
     "pgb_link_grid": ([_vp, _vp, _int, _sz, _P(abi.LinkRadiiC), _P(_sz)], _int),
     "pgb_fetch_clusters": ([_vp, _vp, _sz, _vp, _sz], _int),
     "pgb_search_file_u8": ([_vp, _vp, _int, _u64, _vp, _sz, _P(abi.EngineConfigC),
-                            _P(abi.LinkRadiiC), _P(_sz), _P(_sz)], _int),
+                            _P(abi.LinkRadiiC), _P(abi.RfiConfigC), _P(_sz), _P(_sz)], _int),
+    "pgb_rfi_clean": ([_vp, _vp, _int, _int, _u64, _P(abi.RfiConfigC), _vp, _P(_u64), _P(_u64)], _int),
+    "pgb_fetch_rfi_flags": ([_vp, _vp, _vp], _int),
     "pgb_fetch_file_candidates": ([_vp, _vp, _sz], _int),
     "pgb_fetch_file_skipped": ([_vp, _vp, _sz, _P(_sz)], _int),
     "pgb_launch_count": ([_vp, _P(_u64)], _int),

@@ -44,6 +44,7 @@ ERR_BUDGET = 4
 ERR_DEGENERATE = 5
 ERR_INVALID_PLAN = 6
 ERR_ARGUMENT = 7
+ERR_INSUFFICIENT = 8
 ERR_NO_DEVICE = 100
 ERR_CUDA = 101
 ERR_OOM = 102
@@ -68,6 +69,12 @@ class EngineConfigC(ctypes.Structure):
 class LinkRadiiC(ctypes.Structure):
     _fields_ = [("sep_time", ctypes.c_uint64), ("sep_dm_trials", ctypes.c_uint32),
                 ("sep_width", ctypes.c_uint32)]
+
+
+class RfiConfigC(ctypes.Structure):
+    _fields_ = [("narrowband", ctypes.c_int32), ("broadband", ctypes.c_int32),
+                ("k_sigma", ctypes.c_double), ("k_mad", ctypes.c_double),
+                ("local_mean", ctypes.c_int32), ("_pad", ctypes.c_int32)]
 
 
 class HeaderC(ctypes.Structure):

@@ -117,6 +117,9 @@ struct pgb_context {
     DevBuf file_cands, file_sorted;
     DevBuf cl_scratch, clusters, members;
     PinnedBuf h_counters;
+    RfiWork rfi;
+    DevBuf rfi_out;
+    uint64_t rfi_len = 0;
 
     uint64_t cand_cap = 1 << 16, frag_cap = 1 << 16;
 
@@ -456,6 +459,31 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     ctx->last_u8 = u8;
 }
 
+// A float chunk whose cells are all integers in [0, 255] (read_chunk's widening of
+// 8-bit data, src/filterbank.cpp:304-307, or a zero-policy RFI mask) takes the integer
+// path: every in-order fp32 partial sum is then an exact integer, so series and
+// baselines are bit-identical.  Repacked on the device; otherwise the fp32 path.
+ChunkInput prepare_f32(pgb_context* ctx, const float* dptr, uint64_t length) {
+    if (!ctx->ntrials || !length || getenv("PGB_FORCE_F32_PATH")) return ChunkInput{dptr, false};
+    const size_t cells = (size_t)length * ctx->nchans;
+    ctx->in_u8.reserve(cells);
+    ctx->counters.reserve(4 * sizeof(unsigned long long));
+    ctx->h_counters.reserve(4 * sizeof(unsigned long long));
+    auto* dflag = ctx->counters.as<unsigned long long>() + 2;
+    PGB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(unsigned long long), ctx->st));
+    launch_pack_u8(dptr, cells, ctx->in_u8.as<uint8_t>(), dflag, ctx->st);
+    auto* hflag = ctx->h_counters.as<unsigned long long>() + 2;
+    PGB_CUDA(cudaMemcpyAsync(hflag, dflag, sizeof *hflag, cudaMemcpyDeviceToHost, ctx->st));
+    PGB_CUDA(cudaStreamSynchronize(ctx->st));
+    ctx->launches += 1;
+    if (*hflag == 0) return ChunkInput{ctx->in_u8.p, true};
+    return ChunkInput{dptr, false};
+}
+
+RfiParams to_rfi(const pgb_rfi_config* r) {
+    return RfiParams{r->narrowband, r->broadband, r->local_mean, r->k_sigma, r->k_mad};
+}
+
 void reset_timing(pgb_context* ctx) {
     ctx->dedisp_ms = 0.0;
     ctx->dedisp_launches = 0;
@@ -564,7 +592,8 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         cudaStreamSynchronize(ctx->copy_st);
         for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,
                           &ctx->base, &ctx->frms, &ctx->status, &ctx->d_active, &ctx->d_row_len,
-                          &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->ws_base, &ctx->ws_off, &ctx->cands_raw, &ctx->cands_sorted,
+                          &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->ws_base, &ctx->ws_off, &ctx->rfi_out, &ctx->rfi.chan_bad,
+                          &ctx->rfi.samp_bad, &ctx->rfi.dbl, &ctx->rfi.tmp, &ctx->rfi.rows, &ctx->cands_raw, &ctx->cands_sorted,
                           &ctx->frags, &ctx->frags_sorted, &ctx->counters, &ctx->sort_keys,
                           &ctx->sort_idx, &ctx->sort_tmp, &ctx->payload, &ctx->file_cands,
                           &ctx->file_sorted, &ctx->cl_scratch, &ctx->clusters, &ctx->members})
@@ -642,29 +671,9 @@ static pgb_status run_dm_loop_impl(pgb_context* ctx, const void* data, bool u8, 
             PGB_CUDA(cudaMemcpyAsync(ctx->in_raw.p, data, bytes, cudaMemcpyHostToDevice, ctx->st));
             dptr = ctx->in_raw.p;
         }
-        bool as_u8 = u8;
-        if (!u8 && ctx->ntrials && spec->length && !getenv("PGB_FORCE_F32_PATH")) {
-            // Widened 8-bit chunks (read_chunk, src/filterbank.cpp:304-307) hold integers in
-            // [0, 255]: every in-order fp32 partial sum is then an exact integer, so the
-            // integer path gives bit-identical series and baselines.  Repack on the device.
-            const size_t cells = (size_t)spec->length * ctx->nchans;
-            ctx->in_u8.reserve(cells);
-            ctx->counters.reserve(4 * sizeof(unsigned long long));
-            ctx->h_counters.reserve(4 * sizeof(unsigned long long));
-            auto* dflag = ctx->counters.as<unsigned long long>() + 2;
-            PGB_CUDA(cudaMemsetAsync(dflag, 0, sizeof(unsigned long long), ctx->st));
-            launch_pack_u8(static_cast<const float*>(dptr), cells, ctx->in_u8.as<uint8_t>(), dflag,
-                           ctx->st);
-            auto* hflag = ctx->h_counters.as<unsigned long long>() + 2;
-            PGB_CUDA(cudaMemcpyAsync(hflag, dflag, sizeof *hflag, cudaMemcpyDeviceToHost, ctx->st));
-            PGB_CUDA(cudaStreamSynchronize(ctx->st));
-            ctx->launches += 1;
-            if (*hflag == 0) {
-                dptr = ctx->in_u8.p;
-                as_u8 = true;
-            }
-        }
-        run_chunk(ctx, ChunkInput{dptr, as_u8}, spec, cfg);
+        const ChunkInput ci = u8 ? ChunkInput{dptr, true}
+                                 : prepare_f32(ctx, static_cast<const float*>(dptr), spec->length);
+        run_chunk(ctx, ci, spec, cfg);
         if (n_candidates) *n_candidates = ctx->n_cands;
         if (n_skipped) *n_skipped = ctx->skipped.size();
     });
@@ -778,6 +787,49 @@ pgb_status pgb_dedisperse_f32(pgb_context* ctx, const float* data, uint64_t leng
     return dedisperse_impl(ctx, data, false, length, trial_begin, trial_end, out, out_stride);
 }
 
+pgb_status pgb_rfi_clean(pgb_context* ctx, const void* data, int is_u8, int on_device,
+                         uint64_t length, const pgb_rfi_config* rfi, float* out_host,
+                         uint64_t* n_bad_channels, uint64_t* n_bad_samples) {
+    return guarded([&] {
+        need(ctx && data && rfi && ctx->nchans, PGB_ERR_ARGUMENT, "null argument or no plan");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        const uint32_t C = ctx->nchans;
+        const size_t cells = (size_t)length * C;
+        const void* dptr = data;
+        if (!on_device) {
+            ctx->in_raw.reserve(cells * (is_u8 ? 1 : 4));
+            PGB_CUDA(cudaMemcpyAsync(ctx->in_raw.p, data, cells * (is_u8 ? 1 : 4), cudaMemcpyHostToDevice,
+                                     ctx->st));
+            dptr = ctx->in_raw.p;
+        }
+        ctx->rfi_out.reserve(cells * 4);
+        uint64_t nbc = 0, nbs = 0;
+        if (is_u8)
+            rfi_clean_impl<uint8_t>(static_cast<const uint8_t*>(dptr), length, C, to_rfi(rfi), ctx->rfi,
+                                    ctx->rfi_out.as<float>(), ctx->st, &nbc, &nbs);
+        else
+            rfi_clean_impl<float>(static_cast<const float*>(dptr), length, C, to_rfi(rfi), ctx->rfi,
+                                  ctx->rfi_out.as<float>(), ctx->st, &nbc, &nbs);
+        ctx->rfi_len = length;
+        if (out_host)
+            PGB_CUDA(cudaMemcpyAsync(out_host, ctx->rfi_out.p, cells * 4, cudaMemcpyDeviceToHost, ctx->st));
+        PGB_CUDA(cudaStreamSynchronize(ctx->st));
+        if (n_bad_channels) *n_bad_channels = nbc;
+        if (n_bad_samples) *n_bad_samples = nbs;
+    });
+}
+
+pgb_status pgb_fetch_rfi_flags(pgb_context* ctx, uint8_t* bad_channels, uint8_t* bad_samples) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        if (bad_channels && ctx->rfi.chan_bad.p)
+            PGB_CUDA(cudaMemcpyAsync(bad_channels, ctx->rfi.chan_bad.p, ctx->nchans, cudaMemcpyDeviceToHost, ctx->st));
+        if (bad_samples && ctx->rfi.samp_bad.p)
+            PGB_CUDA(cudaMemcpyAsync(bad_samples, ctx->rfi.samp_bad.p, ctx->rfi_len, cudaMemcpyDeviceToHost, ctx->st));
+        PGB_CUDA(cudaStreamSynchronize(ctx->st));
+    });
+}
+
 pgb_status pgb_link_grid(pgb_context* ctx, const pgb_candidate* cands, int on_device, size_t n,
                          const pgb_link_radii* radii, size_t* n_clusters) {
     return guarded([&] {
@@ -820,7 +872,7 @@ pgb_status pgb_fetch_clusters(pgb_context* ctx, pgb_cluster* out, size_t capacit
 pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payload_on_device,
                               uint64_t nsamples, const pgb_chunk_spec* chunks, size_t nchunks,
                               const pgb_engine_config* cfg, const pgb_link_radii* radii,
-                              size_t* n_candidates, size_t* n_clusters) {
+                              const pgb_rfi_config* rfi, size_t* n_candidates, size_t* n_clusters) {
     return guarded([&] {
         need(ctx && payload && cfg && (nchunks == 0 || chunks), PGB_ERR_ARGUMENT,
              "null argument");
@@ -856,7 +908,17 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
         for (size_t k = 0; k < nchunks; ++k) {
             validate_cfg(ctx, &chunks[k], cfg);
             if (!payload_on_device) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
-            run_chunk(ctx, ChunkInput{dpay + chunks[k].start_sample * C, true}, &chunks[k], cfg);
+            const uint8_t* cptr = dpay + chunks[k].start_sample * C;
+            ChunkInput ci{cptr, true};
+            if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
+                uint64_t nbc = 0, nbs = 0;
+                ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);
+                rfi_clean_impl<uint8_t>(cptr, chunks[k].length, C, to_rfi(rfi), ctx->rfi, ctx->rfi_out.as<float>(),
+                                        ctx->st, &nbc, &nbs);
+                ctx->launches += 8;
+                if (nbc || nbs) ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
+            }
+            run_chunk(ctx, ci, &chunks[k], cfg);
             const uint64_t nc = ctx->n_cands;
             if (nc) {
                 if ((total + nc) * sizeof(pgb_candidate) > ctx->file_cands.bytes) {

@@ -150,6 +150,22 @@ void sort_candidates(const pgb_candidate* in, pgb_candidate* out, uint64_t n, vo
                      size_t temp_bytes, uint64_t* keys_a, uint64_t* keys_b, uint32_t* idx_a,
                      uint32_t* idx_b, cudaStream_t st);
 
+// RFI excision (rfi.cu)
+struct RfiParams {
+    int narrowband;
+    int broadband;
+    int local_mean;
+    double k_sigma;
+    double k_mad;
+};
+struct RfiWork {
+    DevBuf chan_bad, samp_bad, dbl, tmp, rows;
+};
+// Flags and masks the time-major chunk x[n][nch] into `out` (float, same layout).
+template <typename T>
+void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w,
+                    float* out, cudaStream_t st, uint64_t* n_bad_ch, uint64_t* n_bad_s);
+
 // clustering
 struct ClusterWork;  // device scratch, defined in cluster.cu
 struct ClusterResultDev {

@@ -78,6 +78,25 @@ class LinkRadii:
 
 
 @dataclass
+class RfiConfig:
+    """The RFI fields of pulsegrid::SearchParams (pipeline.hpp:31-35); reference defaults."""
+
+    narrowband: bool = True
+    broadband: bool = True
+    k_sigma: float = 6.0
+    k_mad: float = 5.0
+    local_mean: bool = True  # MaskPolicy::local_mean (False = zero)
+
+    def _c(self) -> abi.RfiConfigC:
+        return abi.RfiConfigC(int(self.narrowband), int(self.broadband), float(self.k_sigma),
+                              float(self.k_mad), int(self.local_mean), 0)
+
+    @property
+    def active(self) -> bool:
+        return bool(self.narrowband or self.broadband)
+
+
+@dataclass
 class TrialTiming:
     """pulsegrid::TrialTiming (engine.hpp:16-23); device stages are amortized per trial."""
 
@@ -307,7 +326,7 @@ class Engine:
     # ---- file-level search ------------------------------------------------------------
     def search_file(self, payload, nsamples: int, chunks: list[ChunkSpec], plan: DmTrialPlan,
                     cfg: EngineConfig, *, trial_range: tuple[int, int] | None = None,
-                    cluster: bool = True):
+                    cluster: bool = True, rfi: RfiConfig | None = None):
         """execute_task's chunk loop + sort + link_grid on a raw 8-bit payload.
 
         Returns (candidates, clusters, skipped (chunk, trial) pairs).  cluster=False
@@ -329,9 +348,31 @@ class Engine:
         else:
             payload = np.ascontiguousarray(payload, dtype=np.uint8)
             ptr, on_dev = abi.ptr(payload), 0
+        rc = rfi._c() if (rfi is not None and rfi.active) else None
         check(lib.pgb_search_file_u8(self._h, ptr, on_dev, int(nsamples), abi.ptr(arr), len(arr),
-                                     ctypes.byref(ccfg), rp, ctypes.byref(nc), ctypes.byref(ncl)))
+                                     ctypes.byref(ccfg), rp, ctypes.byref(rc) if rc is not None else None,
+                                     ctypes.byref(nc), ctypes.byref(ncl)))
         return self.fetch_file_results(nc.value, ncl.value)
+
+    # ---- RFI excision --------------------------------------------------------------------
+    def rfi_clean(self, chunk_data: np.ndarray, plan: DmTrialPlan, rfi: RfiConfig):
+        """flag_narrowband + flag_broadband + apply_mask (src/rfi.cpp:32-139) on one chunk.
+
+        Returns (cleaned float chunk, bad-channel mask, bad-sample mask)."""
+        self.set_plan(plan)
+        data = np.asarray(chunk_data)
+        is_u8 = data.dtype == np.uint8
+        data = np.ascontiguousarray(data, dtype=np.uint8 if is_u8 else np.float32)
+        L, nch = data.shape
+        out = np.zeros((L, nch), np.float32)
+        rc = rfi._c()
+        nbc, nbs = ctypes.c_uint64(), ctypes.c_uint64()
+        check(lib.pgb_rfi_clean(self._h, abi.ptr(data), int(is_u8), 0, L, ctypes.byref(rc), abi.ptr(out),
+                                ctypes.byref(nbc), ctypes.byref(nbs)))
+        bc = np.zeros(nch, np.uint8)
+        bs = np.zeros(L, np.uint8)
+        check(lib.pgb_fetch_rfi_flags(self._h, abi.ptr(bc), abi.ptr(bs)))
+        return out, bc.astype(bool), bs.astype(bool)
 
     def fetch_file_results(self, nc: int, ncl: int):
         cands = np.zeros(nc, abi.CANDIDATE_DTYPE)

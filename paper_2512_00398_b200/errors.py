@@ -39,6 +39,10 @@ class InvalidPlanError(PulsegridError):
     """pulsegrid::invalid_plan_error (errors.hpp:24-26)."""
 
 
+class InsufficientStatisticsError(PulsegridError):
+    """pulsegrid::insufficient_statistics_error (errors.hpp:40-42)."""
+
+
 class DeviceError(PulsegridError):
     """No usable sm_100 device, a CUDA failure, or device OOM (no CPU fallback exists)."""
 
@@ -51,6 +55,7 @@ _BY_CODE = {
     5: DegenerateSeriesError,
     6: InvalidPlanError,
     7: ValueError,
+    8: InsufficientStatisticsError,
     100: DeviceError,
     101: DeviceError,
     102: DeviceError,

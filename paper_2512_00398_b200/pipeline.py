@@ -7,8 +7,9 @@ exactly like the reference; `search_file` then runs every chunk on the device
 sorts all candidates and clusters them with link_grid without leaving the GPU;
 `write_candidates` produces the reference's .cand text (src/cluster_io.cpp:11-34).
 
-RFI excision (src/rfi.cpp) runs upstream of the path and is not part of this
-package; searches here correspond to the reference with `--no-rfi-*`.
+RFI excision (src/rfi.cpp, next row f1) runs on the device before each chunk's
+DM loop when enabled (`SearchParams.rfi`, reference defaults: both flaggers on,
+local-mean replacement).
 """
 from __future__ import annotations
 
@@ -20,7 +21,7 @@ from pathlib import Path
 import numpy as np
 
 from .dedisp import DmTrialPlan, FilterbankHeader, LinearSpacing, AdaptiveSpacing, generate_dm_trials
-from .engine import ChunkSpec, EngineConfig, default_engine
+from .engine import ChunkSpec, EngineConfig, RfiConfig, default_engine
 from .cluster import Clusters
 
 
@@ -67,6 +68,7 @@ class SearchParams:
     engine: EngineConfig = field(default_factory=EngineConfig)
     baseline_len_s: float = 2.0
     nsamps_chunk: int = 1 << 18
+    rfi: RfiConfig = field(default_factory=RfiConfig)  # reference default: both flaggers on
 
 
 @dataclass
@@ -77,6 +79,7 @@ class SearchTask:
     plan: DmTrialPlan
     engine: EngineConfig
     chunks: list[ChunkSpec]
+    rfi: RfiConfig = field(default_factory=lambda: RfiConfig(False, False))
 
 
 def create_task(header: FilterbankHeader, params: SearchParams) -> SearchTask:
@@ -94,7 +97,7 @@ def create_task(header: FilterbankHeader, params: SearchParams) -> SearchTask:
     if chunk_len <= overlap or header.nsamples <= overlap:
         chunk_len = header.nsamples
     chunks = plan_chunks(header.nsamples, chunk_len, 0 if chunk_len >= header.nsamples else overlap)
-    return SearchTask(header, plan, eng, chunks)
+    return SearchTask(header, plan, eng, chunks, params.rfi)
 
 
 @dataclass
@@ -109,7 +112,8 @@ def search_file(payload: np.ndarray, task: SearchTask, *, device: int = 0,
     """execute_task's loop (src/pipeline.cpp:72-106) on a [nsamples][nchans] u8 payload."""
     eng = default_engine(device)
     cands, clusters, skipped = eng.search_file(payload, task.header.nsamples, task.chunks,
-                                               task.plan, task.engine, trial_range=trial_range)
+                                               task.plan, task.engine, trial_range=trial_range,
+                                               rfi=task.rfi)
     return SearchResult(cands, clusters, skipped)
 
 

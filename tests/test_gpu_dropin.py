@@ -15,7 +15,7 @@ import numpy as np
 import pytest
 
 from paper_2512_00398_b200.dedisp import LinearSpacing
-from paper_2512_00398_b200.engine import EngineConfig
+from paper_2512_00398_b200.engine import EngineConfig, RfiConfig
 from paper_2512_00398_b200.pipeline import SearchParams, create_task, read_filterbank, search_file, write_candidates
 
 pytestmark = pytest.mark.gpu
@@ -62,7 +62,7 @@ def test_link_substitution_u8(ref, tmp_path):
     hdr, payload = read_filterbank(fil)
     params = SearchParams(dm_lo=ARGS_U8[0], dm_hi=ARGS_U8[1], spacing=LinearSpacing(ARGS_U8[2]),
                           engine=EngineConfig(boxcar_max=ARGS_U8[3]), baseline_len_s=ARGS_U8[4],
-                          nsamps_chunk=ARGS_U8[5])
+                          nsamps_chunk=ARGS_U8[5], rfi=RfiConfig(False, False))
     res = search_file(payload, create_task(hdr, params))
     assert write_candidates(res.clusters) == ref_text
 
