@@ -251,12 +251,20 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     from paper_2512_00398_b200.distributed import gather_candidates, shard_trials, trial_work
     from paper_2512_00398_b200.engine import Engine
 
+    # PG_DIST_BACKEND=gloo + PG_SAME_GPU=1 exercise the multi-rank path on one GPU
+    # (functional check only: ranks then share the device and the timing is meaningless)
+    backend = os.environ.get("PG_DIST_BACKEND", "nccl")
+    if os.environ.get("PG_SAME_GPU"):
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     task = build_task(cfg)
     plan = task.plan
     t0 = time.time()
@@ -275,7 +283,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
                                              trial_range=(lo, hi), cluster=(world == 1))
         d2h = cands.nbytes + (clusters.records.nbytes + clusters.members.nbytes if world == 1 else 0)
         if world > 1:
-            merged = gather_candidates(cands, device=dev)
+            merged = gather_candidates(cands, device=dev if backend == "nccl" else torch.device("cpu"))
             if rank == 0:
                 cl = eng.link_grid(merged, task.engine.radii)
                 d2h += cl.records.nbytes + cl.members.nbytes
@@ -303,7 +311,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             dist.barrier()
         el = ev0.elapsed_time(ev1)
         if dist:
-            t = torch.tensor([el], dtype=torch.float64, device=dev)
+            t = torch.tensor([el], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
         return el, d2h // steps, eng.launch_count() - launches0, dd_ms, dd_n, dd_adds
