@@ -348,6 +348,9 @@ class Engine:
         else:
             payload = np.ascontiguousarray(payload, dtype=np.uint8)
             ptr, on_dev = abi.ptr(payload), 0
+        shape = tuple(payload.shape)
+        if len(shape) != 2 or shape[1] != plan.nchans or shape[0] < nsamples:
+            raise ValueError(f"payload of shape {shape} does not hold {nsamples} x {plan.nchans} samples")
         rc = rfi._c() if (rfi is not None and rfi.active) else None
         check(lib.pgb_search_file_u8(self._h, ptr, on_dev, int(nsamples), abi.ptr(arr), len(arr),
                                      ctypes.byref(ccfg), rp, ctypes.byref(rc) if rc is not None else None,

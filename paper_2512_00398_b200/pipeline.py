@@ -117,6 +117,33 @@ def search_file(payload: np.ndarray, task: SearchTask, *, device: int = 0,
     return SearchResult(cands, clusters, skipped)
 
 
+def run_multi_file(payloads: list[np.ndarray], tasks: list[SearchTask], *, n_exec: int = 4,
+                   device: int = 0) -> list[SearchResult | Exception]:
+    """Multi-file execution (src/pipeline.cpp:136-210, next row f3) on one GPU.
+
+    The reference overlaps task creation and execution with two bounded queues of
+    worker threads; here `n_exec` host threads each own a device context (its own
+    CUDA stream and arena, `default_engine` is per thread), so several files'
+    uploads, kernels and syncs interleave on the GPU.  Results are in submission
+    order; a failing file yields its exception instead of a result (per-file
+    isolation, src/pipeline.cpp:173-192)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    if n_exec < 1:
+        from .errors import ConfigError
+
+        raise ConfigError("need at least one worker per stage")
+
+    def one(k):
+        try:
+            return search_file(payloads[k], tasks[k], device=device)
+        except Exception as exc:  # isolate-and-continue
+            return exc
+
+    with ThreadPoolExecutor(n_exec) as ex:
+        return list(ex.map(one, range(len(tasks))))
+
+
 def write_candidates(clusters: Clusters) -> str:
     """src/cluster_io.cpp:11-34: one line per cluster, sorted by (peak_sample, dm_trial)."""
     recs = clusters.records
