@@ -113,7 +113,8 @@ struct pgb_context {
     // device work buffers
     DevBuf in_raw, rows, series, base, frms, status, d_active, d_row_len, d_blk_len, d_scale;
     DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
-    DevBuf payload, in_u8, ws_base, ws_off;
+    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off;
+    uint32_t dd_tab_wmax = 0;  // wmax the staging table was built for (0 = stale)
     DevBuf file_cands, file_sorted;
     DevBuf cl_scratch, clusters, members;
     PinnedBuf h_counters;
@@ -248,6 +249,7 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
         }
         ctx->active = active;
         ctx->geom_valid = true;
+        ctx->dd_tab_wmax = 0;
         ctx->d_active.reserve(nrows * sizeof(uint32_t));
         PGB_CUDA(cudaMemcpyAsync(ctx->d_active.p, active.data(), nrows * sizeof(uint32_t),
                                  cudaMemcpyHostToDevice, st));
@@ -289,7 +291,8 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
         round_up((uint64_t)ntiles * DD_NT + maxd_active + std::max(wmax, ws_wmax) + 64, 64);
     const size_t esz = u8 ? 1 : 4;
 
-    ctx->rows.reserve((size_t)C * rows_pitch * esz, true);
+    const uint32_t C_pad = (C + 7) & ~7u;  // u8 rows padded with zero rows to whole 8-channel groups
+    ctx->rows.reserve((size_t)(u8 ? C_pad : C) * rows_pitch * esz, true);
     ctx->series.reserve((size_t)nrows * out_pitch * 4);
     const bool baseline = cfg->baseline_window > 0;
     if (baseline) ctx->base.reserve((size_t)nrows * out_pitch * 4);
@@ -310,9 +313,13 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     }
 
     // 1. transpose to channel-major rows
-    if (u8)
+    if (u8) {
         launch_transpose_u8(static_cast<const uint8_t*>(in.data), L, C, ctx->rows.as<uint8_t>(),
                             rows_pitch, st);
+        if (C_pad > C)
+            PGB_CUDA(cudaMemsetAsync(ctx->rows.as<uint8_t>() + (size_t)C * rows_pitch, 0,
+                                     (size_t)(C_pad - C) * rows_pitch, st));
+    }
     else
         launch_transpose_f32(static_cast<const float*>(in.data), L, C, ctx->rows.as<float>(),
                              rows_pitch, st);
@@ -345,8 +352,19 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
         launch_ws_offsets(dw, ctx->ws_base.as<uint32_t>(), ctx->ws_off.as<uint16_t>(), st);
         ctx->launches += 1;
         launch_dedisp_u8_ws(dw, ws_ns, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
-    } else if (u8)
+    } else if (u8) {
+        dl.nchans_pad = C_pad;
+        if (ctx->dd_tab_wmax != wmax) {
+            ctx->dd_win.reserve((size_t)nblocks * dl.nchans_pad * sizeof(uint2));
+            ctx->dd_off.reserve((size_t)nblocks * dl.nchans_pad * 32 * 4);
+            launch_dd_table(dl, ctx->dd_win.as<uint2>(), ctx->dd_off.as<uint32_t>(), st);
+            ctx->launches += 1;
+            ctx->dd_tab_wmax = wmax;
+        }
+        dl.dd_win = ctx->dd_win.as<uint2>();
+        dl.dd_off = ctx->dd_off.as<uint32_t>();
         launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+    }
     else launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
     PGB_CUDA(cudaEventRecord(ctx->ev_dd1, st));
     ctx->dedisp_launches += 1;
@@ -592,7 +610,7 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         cudaStreamSynchronize(ctx->copy_st);
         for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,
                           &ctx->base, &ctx->frms, &ctx->status, &ctx->d_active, &ctx->d_row_len,
-                          &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->ws_base, &ctx->ws_off, &ctx->rfi_out, &ctx->rfi.chan_bad,
+                          &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->ws_base, &ctx->ws_off, &ctx->dd_win, &ctx->dd_off, &ctx->rfi_out, &ctx->rfi.chan_bad,
                           &ctx->rfi.samp_bad, &ctx->rfi.dbl, &ctx->rfi.tmp, &ctx->rfi.rows, &ctx->cands_raw, &ctx->cands_sorted,
                           &ctx->frags, &ctx->frags_sorted, &ctx->counters, &ctx->sort_keys,
                           &ctx->sort_idx, &ctx->sort_tmp, &ctx->payload, &ctx->file_cands,

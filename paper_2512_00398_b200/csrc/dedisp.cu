@@ -264,6 +264,195 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     }
 }
 
+// Tile-independent staging geometry of the u8 kernel, one warp per (trial block,
+// channel): the window of channel c for a block starts at i0 + (min_t d_t(c) & ~15)
+// (i0 is a multiple of DD_NT, so 16-byte aligned) and trial t reads it at
+// o_t = d_t(c) - start, i.e. at byte (o_t & 3) * W + (o_t >> 2) * 4 of the channel's
+// 4-copy slot.  Vectors: enough 16-byte groups for the furthest trial's 1024 bytes.
+__global__ void dd_table_kernel(const DedispLaunch p, uint2* __restrict__ win, uint32_t* __restrict__ off) {
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t blk = gw / p.nchans_pad, c = gw % p.nchans_pad;
+    const uint32_t nblocks = (p.nrows + 31) / 32;
+    if (blk >= nblocks) return;
+    const uint32_t row0 = blk * 32, nrows_blk = min(32u, p.nrows - row0);
+    const uint32_t row = row0 + min((uint32_t)lane, nrows_blk - 1);
+    // channels past nchans are zero rows (the kernel always runs whole 8-channel groups)
+    const uint32_t d = c < p.nchans ? (uint32_t)__ldg(p.delays_ct + (size_t)c * p.ntrials_plan + p.active[row]) : 0;
+    const uint32_t dmin = warp_min_u32(d), dmax = warp_max_u32(d);
+    const uint32_t a = dmin & ~15u;
+    const uint32_t o = d - a;
+    off[(size_t)gw * 32 + lane] = (o & 3) * p.wmax + (o >> 2) * 4;
+    if (lane == 0)
+        win[gw] = make_uint2(a, (((dmax - a) & ~3u) + DD_NT - 1) / 16 + 1);
+}
+
+// Table-driven u8 kernel (default).  Same tile, staging layout and SWAR accumulation as
+// dedisp_u8_kernel<.., 3>, but the per-stage offsets come from dd_table_kernel:
+//   * the per-trial offsets of stage g+1 are copied into shared memory with cp.async
+//     while stage g computes (no per-stage delay loads, shuffles or offset math);
+//   * each channel stages only its own window (min..max delay of the block + 1024),
+//     not the widest channel's;
+//   * one barrier per stage;
+//   * G (channels per stage) and VPT (16-byte vectors per staging thread) are compile
+//     time and the channel rows are padded with zero rows to a multiple of 8, so a
+//     stage is straight-line code (no loop-carried register shuffles, no dead
+//     predicated loads).
+template <int G, int VPT>
+__global__ void __launch_bounds__(DD_THREADS, 1)
+    dedisp_u8_tab_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
+                         int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    constexpr int TPW = 2;
+    constexpr int TB = DD_WARPS * TPW;
+    static_assert(TB == 32, "table layout assumes 32-trial blocks");
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t W = p.wmax;  // bytes per copy
+    uint8_t* buf = smem;                                                          // [2][G][4][W]
+    uint32_t* offs = reinterpret_cast<uint32_t*>(smem + (size_t)2 * G * 4 * W);  // [2][G][TB]
+
+    const uint32_t blk = blockIdx.x;
+    const uint32_t row0 = blk * TB;
+    const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
+    const uint64_t i0 = (uint64_t)blockIdx.y * DD_NT;
+    if (i0 >= blk_len[blk]) return;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nstages = p.nchans_pad / G;
+    constexpr int wpc = DD_WARPS / G;
+    const int my_cs = warp / wpc;
+    const uint32_t my_t = (uint32_t)((warp % wpc) * 32 + lane);
+    constexpr uint32_t vstride = (uint32_t)wpc * 32;
+    const uint32_t* offtab = p.dd_off + (size_t)blk * p.nchans_pad * TB;
+    const uint2* wintab = p.dd_win + (size_t)blk * p.nchans_pad;
+    const uint8_t* rows_i0 = rows + i0;
+
+    uint4 v0[VPT];
+    uint32_t v1[VPT];
+
+    auto fetch_offs = [&](uint32_t gi, int b) {
+        if ((int)threadIdx.x < G * TB / 4)
+            __pipeline_memcpy_async(offs + b * G * TB + 4 * threadIdx.x,
+                                    offtab + (size_t)gi * G * TB + 4 * threadIdx.x, 16);
+        __pipeline_commit();
+    };
+    auto load_stage = [&](uint32_t gi, uint2 wv) {
+        const uint8_t* src = rows_i0 + (size_t)(gi * G + my_cs) * p.rows_pitch + wv.x;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const uint32_t vi = my_t + k * vstride;
+            if (vi < wv.y) {
+                v0[k] = __ldg(reinterpret_cast<const uint4*>(src + 16 * vi));
+                v1[k] = __ldg(reinterpret_cast<const uint32_t*>(src + 16 * vi + 16));
+            }
+        }
+    };
+    auto store_stage = [&](int b, uint2 wv) {
+        uint8_t* base = buf + (size_t)((b * G + my_cs) * 4) * W;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const uint32_t vi = my_t + k * vstride;
+            if (vi < wv.y) {
+                uint8_t* dst = base + 16 * vi;
+                const uint32_t w[5] = {v0[k].x, v0[k].y, v0[k].z, v0[k].w, v1[k]};
+                *reinterpret_cast<uint4*>(dst) = v0[k];
+#pragma unroll
+                for (int s = 1; s < 4; ++s) {
+                    const uint32_t sel = (uint32_t)(s | (s + 1) << 4 | (s + 2) << 8 | (s + 3) << 12);
+                    uint4 sh;
+                    sh.x = __byte_perm(w[0], w[1], sel);
+                    sh.y = __byte_perm(w[1], w[2], sel);
+                    sh.z = __byte_perm(w[2], w[3], sel);
+                    sh.w = __byte_perm(w[3], w[4], sel);
+                    *reinterpret_cast<uint4*>(dst + (size_t)s * W) = sh;
+                }
+            }
+        }
+    };
+
+    uint32_t E[TPW][DD_WORDS], H[TPW][DD_WORDS];
+    const uint32_t one = p.mul24 >> 24;  // 1, opaque to the compiler (keeps E on IMAD)
+#pragma unroll
+    for (int u = 0; u < TPW; ++u)
+#pragma unroll
+        for (int m = 0; m < DD_WORDS; ++m) E[u][m] = H[u][m] = 0;
+    bool first_flush = true;
+
+    auto flush = [&]() {
+#pragma unroll
+        for (int u = 0; u < TPW; ++u) {
+            const uint32_t r = warp * TPW + u;
+            if (r < nrows_blk) {
+                int32_t* dst = out + (size_t)(row0 + r) * p.out_pitch + i0;
+#pragma unroll
+                for (int m = 0; m < DD_WORDS; ++m) {
+                    const uint32_t e = E[u][m];
+                    const uint32_t b0 = e & 0xffffu, b2 = e >> 16;
+                    const uint32_t t = H[u][m] - (b2 << 8);  // B1 + 2^16 B3
+                    int4 val = make_int4((int)b0, (int)(t & 0xffffu), (int)b2, (int)(t >> 16));
+                    int4* pd = reinterpret_cast<int4*>(dst + 4 * (lane + 32 * m));
+                    if (!first_flush) {
+                        const int4 old = *pd;
+                        val.x += old.x;
+                        val.y += old.y;
+                        val.z += old.z;
+                        val.w += old.w;
+                    }
+                    *pd = val;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < DD_WORDS; ++m) E[u][m] = H[u][m] = 0;
+        }
+        first_flush = false;
+    };
+
+    // prologue: stage 0 offsets and data; stage 1 window in flight
+    uint2 wnext = __ldg(wintab + my_cs);
+    fetch_offs(0, 0);
+    load_stage(0, wnext);
+    store_stage(0, wnext);
+    wnext = nstages > 1 ? __ldg(wintab + G + my_cs) : make_uint2(0, 0);
+    __pipeline_wait_prior(0);
+    __syncthreads();
+    const uint32_t stages_per_flush = DD_FLUSH_CH / G;
+    uint32_t since_flush = 0;
+
+    for (uint32_t gi = 0; gi < nstages; ++gi) {
+        const int b = gi & 1;
+        const bool more = gi + 1 < nstages;
+        const uint2 wstage = wnext;
+        if (more) {
+            fetch_offs(gi + 1, b ^ 1);
+            load_stage(gi + 1, wstage);
+            if (gi + 2 < nstages) wnext = __ldg(wintab + (size_t)(gi + 2) * G + my_cs);
+        }
+        const uint32_t* offb = offs + b * G * TB + warp * TPW;
+        const uint8_t* bufb = buf + (size_t)b * G * 4 * W + 4 * lane;
+#pragma unroll
+        for (int cs = 0; cs < G; ++cs) {
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                const uint8_t* src = bufb + (size_t)cs * 4 * W + offb[cs * TB + u];
+#pragma unroll
+                for (int m = 0; m < DD_WORDS; ++m) {
+                    const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 128 * m);
+                    uint32_t e = E[u][m];
+                    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(e) : "r"(w & 0x00ff00ffu), "r"(one));
+                    E[u][m] = e;
+                    H[u][m] += __umulhi(w, 1u << 24);
+                }
+            }
+        }
+        if (more) store_stage(b ^ 1, wstage);
+        if (++since_flush == stages_per_flush || !more) {
+            flush();
+            since_flush = 0;
+        }
+        __pipeline_wait_prior(0);
+        __syncthreads();
+    }
+}
+
 template <int TPW>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_f32_kernel(const DedispLaunch p, const float* __restrict__ rows,
@@ -453,6 +642,29 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const char* e = getenv("PGB_DD_HMODE");
         return e ? atoi(e) : 3;
     }();
+    static const bool v1 = [] {  // PGB_DD_V1=1: per-stage offset kernel (ablation)
+        const char* e = getenv("PGB_DD_V1");
+        return e && *e && *e != '0';
+    }();
+    if (!v1 && p.tpw == 2 && p.dd_off) {
+        // vectors per staging thread: ceil(max window vectors / (32 * warps per channel))
+        const uint32_t vstride = 32u * (DD_WARPS / p.g);
+        const int vpt = (int)((p.wmax / 16 + vstride - 1) / vstride);
+#define PGB_TAB(G_, V_)                                                                           \
+    if (p.g == G_ && vpt <= V_) {                                                                 \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_tab_kernel<G_, V_>,                               \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
+        dedisp_u8_tab_kernel<G_, V_><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);    \
+        PGB_CUDA(cudaGetLastError());                                                             \
+        return;                                                                                   \
+    }
+        PGB_TAB(8, 1) PGB_TAB(8, 2) PGB_TAB(8, 4)
+        PGB_TAB(4, 1) PGB_TAB(4, 2) PGB_TAB(4, 4)
+        PGB_TAB(2, 1) PGB_TAB(2, 2) PGB_TAB(2, 4)
+        PGB_TAB(1, 1) PGB_TAB(1, 2) PGB_TAB(1, 4)
+#undef PGB_TAB
+        raise(PGB_ERR_CONFIG, "no dedispersion kernel for this staging geometry");
+    }
 #define PGB_DD(TPW, M)                                                                          \
     do {                                                                                        \
         PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_kernel<TPW, M>,                                 \
@@ -468,6 +680,12 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         PGB_DD(1, 0);
     }
 #undef PGB_DD
+    PGB_CUDA(cudaGetLastError());
+}
+
+void launch_dd_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st) {
+    const uint64_t warps = (uint64_t)((p.nrows + 31) / 32) * p.nchans_pad;
+    dd_table_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(p, win, off);
     PGB_CUDA(cudaGetLastError());
 }
 

@@ -110,8 +110,14 @@ struct DedispLaunch {
     const uint32_t* wbase;      // [nblocks][nchans] 16-byte aligned minimum delay
     const uint16_t* woff;       // [nblocks][nchans_pad][32] delay - wbase
     uint32_t nchans_pad;        // nchans rounded up to 8
+    // table-driven u8 kernel: per (trial block, channel) window start / vector count and
+    // per (block, channel, trial) byte offset into the 4-copy staging layout
+    const uint2* dd_win;        // [nblocks][nchans_pad] {delay min & ~15, 16-byte vectors}
+    const uint32_t* dd_off;     // [nblocks][nchans_pad][32]
 };
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st);
+// builds p.dd_win / p.dd_off for the active set (tile independent; p.wmax = bytes per copy)
+void launch_dd_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st);
 void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st);
 size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax);
 // warp-specialized TMA variant (dedisp_tma.cu); p.wmax (bytes) must be a multiple of 256

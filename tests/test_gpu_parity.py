@@ -24,6 +24,11 @@ DEDISP_CASES = [
     (256, 1500.0, -1.0, 9000, 100.0, 1.0),
     (1024, 1500.0, -0.25, 20000, 500.0, 2.0),
     (4096, 1518.0, -0.0703125, 40000, 2000.0, 40.0),
+    # wide per-block delay spreads: 4 and 2 channels per stage, 3-4 vectors per stager
+    (4096, 1518.0, -0.0703125, 24000, 800.0, 8.0),
+    (4096, 1518.0, -0.0703125, 30000, 1400.0, 14.0),
+    (1, 1500.0, -1.0, 2000, 0.0, 1.0),
+    (517, 1450.0, -0.5, 12000, 400.0, 2.5),
 ]
 
 
