@@ -386,12 +386,19 @@ __global__ void __launch_bounds__(BX_THREADS)
     const uint32_t nin = (uint32_t)(n - i0 < (uint64_t)N ? n - i0 : (uint64_t)N);
     const size_t base = (size_t)row * pitch + i0;
 
+    // all S loads in flight before the first division (the division's slow-path call
+    // would otherwise serialise one global latency per element)
+    float xin[S];
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+        const uint32_t j = tid + BX_THREADS * k;
+        xin[k] = j < nin ? load_x<KIND>(x_all, base + j) : 0.0f;
+    }
     double r[S];
 #pragma unroll
     for (int k = 0; k < S; ++k) {
         const uint32_t j = tid + BX_THREADS * k;
-        double v = 0.0;
-        if (j < nin) v = (double)__fdiv_rn(load_x<KIND>(x_all, base + j), frms);  // :211
+        const double v = j < nin ? (double)__fdiv_rn(xin[k], frms) : 0.0;  // :211
         r[k] = v;
         cur[j] = v;
     }

@@ -298,7 +298,7 @@ __global__ void dd_table_kernel(const DedispLaunch p, uint2* __restrict__ win, u
 //     time and the channel rows are padded with zero rows to a multiple of 8, so a
 //     stage is straight-line code (no loop-carried register shuffles, no dead
 //     predicated loads).
-template <int G, int VPT>
+template <int G, int VPT, int SF>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_u8_tab_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
                          int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
@@ -325,6 +325,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     const uint32_t* offtab = p.dd_off + (size_t)blk * p.nchans_pad * TB;
     const uint2* wintab = p.dd_win + (size_t)blk * p.nchans_pad;
     const uint8_t* rows_i0 = rows + i0;
+    const uint32_t kshift[3] = {p.mul24, p.mul24 >> 8, p.mul24 >> 16};  // 2^24, 2^16, 2^8 (run time)
 
     uint4 v0[VPT];
     uint32_t v1[VPT];
@@ -357,12 +358,25 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
                 *reinterpret_cast<uint4*>(dst) = v0[k];
 #pragma unroll
                 for (int s = 1; s < 4; ++s) {
-                    const uint32_t sel = (uint32_t)(s | (s + 1) << 4 | (s + 2) << 8 | (s + 3) << 12);
                     uint4 sh;
-                    sh.x = __byte_perm(w[0], w[1], sel);
-                    sh.y = __byte_perm(w[1], w[2], sel);
-                    sh.z = __byte_perm(w[2], w[3], sel);
-                    sh.w = __byte_perm(w[3], w[4], sel);
+                    if (SF) {  // funnel shift on the FMA pipe: (lo >> 8s) + hi * 2^(32-8s)
+                        const uint32_t k = kshift[s - 1];
+                        uint32_t q[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint32_t t;
+                            asm("mul.hi.u32 %0, %1, %2;" : "=r"(t) : "r"(w[j]), "r"(k));
+                            asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(t) : "r"(w[j + 1]), "r"(k));
+                            q[j] = t;
+                        }
+                        sh = make_uint4(q[0], q[1], q[2], q[3]);
+                    } else {
+                        const uint32_t sel = (uint32_t)(s | (s + 1) << 4 | (s + 2) << 8 | (s + 3) << 12);
+                        sh.x = __byte_perm(w[0], w[1], sel);
+                        sh.y = __byte_perm(w[1], w[2], sel);
+                        sh.z = __byte_perm(w[2], w[3], sel);
+                        sh.w = __byte_perm(w[3], w[4], sel);
+                    }
                     *reinterpret_cast<uint4*>(dst + (size_t)s * W) = sh;
                 }
             }
@@ -646,23 +660,29 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const char* e = getenv("PGB_DD_V1");
         return e && *e && *e != '0';
     }();
+    static const int sf = [] {  // PGB_DD_SFMA=1: staging shifts on the FMA pipe (ablation)
+        const char* e = getenv("PGB_DD_SFMA");
+        return e && *e == '1' ? 1 : 0;
+    }();
     if (!v1 && p.tpw == 2 && p.dd_off) {
         // vectors per staging thread: ceil(max window vectors / (32 * warps per channel))
         const uint32_t vstride = 32u * (DD_WARPS / p.g);
         const int vpt = (int)((p.wmax / 16 + vstride - 1) / vstride);
-#define PGB_TAB(G_, V_)                                                                           \
-    if (p.g == G_ && vpt <= V_) {                                                                 \
-        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_tab_kernel<G_, V_>,                               \
+#define PGB_TAB3(G_, V_, S_)                                                                      \
+    if (p.g == G_ && vpt <= V_ && sf == S_) {                                                     \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_tab_kernel<G_, V_, S_>,                           \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
-        dedisp_u8_tab_kernel<G_, V_><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);    \
+        dedisp_u8_tab_kernel<G_, V_, S_><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);\
         PGB_CUDA(cudaGetLastError());                                                             \
         return;                                                                                   \
     }
+#define PGB_TAB(G_, V_) PGB_TAB3(G_, V_, 0) PGB_TAB3(G_, V_, 1)
         PGB_TAB(8, 1) PGB_TAB(8, 2) PGB_TAB(8, 4)
         PGB_TAB(4, 1) PGB_TAB(4, 2) PGB_TAB(4, 4)
         PGB_TAB(2, 1) PGB_TAB(2, 2) PGB_TAB(2, 4)
         PGB_TAB(1, 1) PGB_TAB(1, 2) PGB_TAB(1, 4)
 #undef PGB_TAB
+#undef PGB_TAB3
         raise(PGB_ERR_CONFIG, "no dedispersion kernel for this staging geometry");
     }
 #define PGB_DD(TPW, M)                                                                          \
