@@ -63,6 +63,7 @@ __global__ void __launch_bounds__(BL_THREADS)
         for (int64_t i = tid; i < n; i += BL_THREADS) out[i] = __fsub_rn((float)x[i], mean);
         return;
     }
+    const double inv_full = __ddiv_rn(1.0, (double)(2 * h + 1));
     // S_0 = sum x[0..h]
     long long s0 = 0;
     for (int64_t i = tid; i <= h; i += BL_THREADS) s0 += x[i];
@@ -114,7 +115,9 @@ __global__ void __launch_bounds__(BL_THREADS)
             if (i < n) {
                 const int64_t lo = i - h > 0 ? i - h : 0;
                 const int64_t hi = i + h < n - 1 ? i + h : n - 1;
-                const double inv = __ddiv_rn(1.0, (double)(hi - lo + 1));
+                const int64_t cnt = hi - lo + 1;
+                // interior windows share one reciprocal; only the 2h edge samples divide
+                const double inv = cnt == 2 * h + 1 ? inv_full : __ddiv_rn(1.0, (double)cnt);
                 out[i] = __double2float_rn(__fma_rn(-(double)run, inv, (double)xv[k]));
             }
         }
@@ -235,13 +238,15 @@ __global__ void __launch_bounds__(32)
                     const float f = t[j + 4 * u];
                     v[u] = KIND == 1 ? (float)__float_as_int(f) : f;
                 }
+                // double(v)*double(v) is exact (24+24 significant bits), so the
+                // reference's a += v*v (one rounding) is exactly one DFMA
 #pragma unroll
                 for (int u = 0; u < 16; ++u) {
-                    const double sq = __dmul_rn((double)v[u], (double)v[u]);
+                    const double dv = (double)v[u];
                     if (pass == 0) {
-                        a = __dadd_rn(a, sq);
+                        a = __fma_rn(dv, dv, a);
                     } else if (fabsf(v[u]) <= cut) {
-                        b = __dadd_rn(b, sq);
+                        b = __fma_rn(dv, dv, b);
                         ++kept;
                     }
                 }
