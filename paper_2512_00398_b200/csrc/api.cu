@@ -94,7 +94,8 @@ struct pgb_context {
     int device = 0;
     cudaStream_t st = nullptr;
     cudaStream_t copy_st = nullptr;
-    cudaEvent_t ev_dd0 = nullptr, ev_dd1 = nullptr;
+    cudaStream_t rms_st = nullptr;  // robust RMS of chunk k overlaps the boxcar of chunk k-1
+    cudaEvent_t ev_dd0[2] = {}, ev_dd1[2] = {}, ev_front[2] = {}, ev_rms[2] = {};
     std::vector<cudaEvent_t> seg_events;
 
     // plan
@@ -111,7 +112,10 @@ struct pgb_context {
     bool geom_valid = false;
 
     // device work buffers
-    DevBuf in_raw, rows, series, base, frms, status, d_active, d_row_len, d_blk_len, d_scale;
+    DevBuf in_raw, rows, series, d_active, d_blk_len, d_scale;
+    // per-slot buffers: a chunk's chain state lives in slot k & 1 from its front half
+    // (transpose, dedispersion, baseline, RMS) to its back half (boxcar, runs, order)
+    DevBuf base[2], frms[2], status[2], d_row_len[2], slot_active[2];
     DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
     DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off;
     uint32_t dd_tab_wmax = 0;  // wmax the staging table was built for (0 = stale)
@@ -199,22 +203,41 @@ void validate_cfg(pgb_context* ctx, const pgb_chunk_spec* spec, const pgb_engine
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
 
-// Runs the whole chain for one chunk whose samples are already on the device.
-void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spec,
-               const pgb_engine_config* cfg) {
+// One chunk's chain, split in two halves so a file search can overlap them across
+// chunks: the front half (transpose, dedispersion, baseline on the main stream; the
+// latency-bound robust RMS on rms_st) and the back half (boxcar ladder, runs,
+// candidate order, degenerate trials).  Everything a back half needs lives in the
+// chunk's slot, so the back half of chunk k-1 may run after the front half of chunk k.
+struct ChunkRun {
+    bool live = false;  // has active rows, i.e. a back half to run
+    int slot = 0;
+    pgb_chunk_spec spec{};
+    pgb_engine_config cfg{};
+    uint32_t nrows = 0;
+    uint64_t out_pitch = 0, max_n = 0;
+    int kind = 0;
+    bool baseline = false, u8 = true;
+    const void* work = nullptr;
+    std::vector<uint32_t> active;
+    std::vector<uint64_t> skipped;  // uncoverable trials (front) + degenerate ones (back)
+};
+
+void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spec,
+                 const pgb_engine_config* cfg, int slot, ChunkRun& run) {
     cudaStream_t st = ctx->st;
     const uint64_t L = spec->length;
     const uint32_t C = ctx->nchans;
-    ctx->n_cands = 0;
-    ctx->skipped.clear();
-    ctx->last_nrows = 0;
+    run = ChunkRun{};
+    run.slot = slot;
+    run.spec = *spec;
+    run.cfg = *cfg;
     if (ctx->ntrials == 0 || L == 0) return;
 
     // active rows: trials whose span fits the chunk (src/engine.cpp:112-118)
-    std::vector<uint32_t> active;
+    std::vector<uint32_t>& active = run.active;
     active.reserve(ctx->tr_end - ctx->tr_begin);
     for (uint32_t t = ctx->tr_begin; t < ctx->tr_end; ++t) {
-        if ((uint64_t)ctx->maxd[t] >= L) ctx->skipped.push_back(t);
+        if ((uint64_t)ctx->maxd[t] >= L) run.skipped.push_back(t);
         else active.push_back(t);
     }
     const uint32_t nrows = (uint32_t)active.size();
@@ -295,12 +318,15 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     ctx->rows.reserve((size_t)(u8 ? C_pad : C) * rows_pitch * esz, true);
     ctx->series.reserve((size_t)nrows * out_pitch * 4);
     const bool baseline = cfg->baseline_window > 0;
-    if (baseline) ctx->base.reserve((size_t)nrows * out_pitch * 4);
-    ctx->frms.reserve(nrows * sizeof(float));
-    ctx->status.reserve(nrows);
-    ctx->d_row_len.reserve(nrows * sizeof(uint32_t));
+    if (baseline) ctx->base[slot].reserve((size_t)nrows * out_pitch * 4);
+    ctx->frms[slot].reserve(nrows * sizeof(float));
+    ctx->status[slot].reserve(nrows);
+    ctx->d_row_len[slot].reserve(nrows * sizeof(uint32_t));
+    ctx->slot_active[slot].reserve(nrows * sizeof(uint32_t));
     ctx->d_blk_len.reserve(nblocks * sizeof(uint32_t));
-    PGB_CUDA(cudaMemcpyAsync(ctx->d_row_len.p, row_len.data(), nrows * sizeof(uint32_t),
+    PGB_CUDA(cudaMemcpyAsync(ctx->d_row_len[slot].p, row_len.data(), nrows * sizeof(uint32_t),
+                             cudaMemcpyHostToDevice, st));
+    PGB_CUDA(cudaMemcpyAsync(ctx->slot_active[slot].p, active.data(), nrows * sizeof(uint32_t),
                              cudaMemcpyHostToDevice, st));
     PGB_CUDA(cudaMemcpyAsync(ctx->d_blk_len.p, blk_len.data(), nblocks * sizeof(uint32_t),
                              cudaMemcpyHostToDevice, st));
@@ -330,7 +356,7 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     dl.nchans = C;
     dl.active = ctx->d_active.as<uint32_t>();
     dl.nrows = nrows;
-    dl.row_len = ctx->d_row_len.as<uint32_t>();
+    dl.row_len = ctx->d_row_len[slot].as<uint32_t>();
     dl.blk_len = ctx->d_blk_len.as<uint32_t>();
     dl.rows_pitch = rows_pitch;
     dl.out_pitch = out_pitch;
@@ -339,7 +365,7 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     dl.wmax = wmax;
     dl.ntiles = ntiles;
     dl.mul24 = 1u << 24;
-    PGB_CUDA(cudaEventRecord(ctx->ev_dd0, st));
+    PGB_CUDA(cudaEventRecord(ctx->ev_dd0[slot], st));
     if (u8 && ws_g) {
         DedispLaunch dw = dl;
         dw.g = ws_g;
@@ -366,30 +392,61 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
         launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
     }
     else launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
-    PGB_CUDA(cudaEventRecord(ctx->ev_dd1, st));
+    PGB_CUDA(cudaEventRecord(ctx->ev_dd1[slot], st));
     ctx->dedisp_launches += 1;
     ctx->launches += 2;
     uint64_t adds = 0;
     for (uint32_t r = 0; r < nrows; ++r) adds += (uint64_t)row_len[r] * C;
     ctx->channel_adds += adds;
 
-    // 3. baseline, 4. robust RMS
+    // 3. baseline, 4. robust RMS (on rms_st: one sequential chain per thread, so it
+    // leaves the SMs nearly idle and overlaps the previous chunk's boxcar)
     const void* work = ctx->series.p;
     int kind = u8 ? 1 : 0;
+    const uint32_t* d_len = ctx->d_row_len[slot].as<uint32_t>();
     if (baseline) {
         const uint64_t w = cfg->baseline_window % 2 == 0 ? cfg->baseline_window + 1 : cfg->baseline_window;
         if (u8)
-            launch_baseline_int(ctx->series.as<int32_t>(), ctx->base.as<float>(),
-                                ctx->d_row_len.as<uint32_t>(), nrows, out_pitch, w, st);
+            launch_baseline_int(ctx->series.as<int32_t>(), ctx->base[slot].as<float>(), d_len, nrows,
+                                out_pitch, w, st);
         else
-            launch_baseline_f32(ctx->series.as<float>(), ctx->base.as<float>(),
-                                ctx->d_row_len.as<uint32_t>(), nrows, out_pitch, w, st);
-        work = ctx->base.p;
+            launch_baseline_f32(ctx->series.as<float>(), ctx->base[slot].as<float>(), d_len, nrows,
+                                out_pitch, w, st);
+        work = ctx->base[slot].p;
         kind = 0;
     }
-    launch_rms(work, kind, ctx->d_row_len.as<uint32_t>(), nrows, out_pitch, ctx->frms.as<float>(),
-               ctx->status.as<uint8_t>(), st);
+    PGB_CUDA(cudaEventRecord(ctx->ev_front[slot], st));
+    PGB_CUDA(cudaStreamWaitEvent(ctx->rms_st, ctx->ev_front[slot], 0));
+    launch_rms(work, kind, d_len, nrows, out_pitch, ctx->frms[slot].as<float>(),
+               ctx->status[slot].as<uint8_t>(), ctx->rms_st);
+    PGB_CUDA(cudaEventRecord(ctx->ev_rms[slot], ctx->rms_st));
     ctx->launches += 5;
+
+    run.live = true;
+    run.nrows = nrows;
+    run.out_pitch = out_pitch;
+    run.max_n = max_n;
+    run.kind = kind;
+    run.baseline = baseline;
+    run.u8 = u8;
+    run.work = work;
+}
+
+void chunk_back(pgb_context* ctx, ChunkRun& run) {
+    cudaStream_t st = ctx->st;
+    const int slot = run.slot;
+    const pgb_chunk_spec* spec = &run.spec;
+    const pgb_engine_config* cfg = &run.cfg;
+    ctx->n_cands = 0;
+    ctx->skipped = run.skipped;
+    ctx->last_nrows = 0;
+    if (!run.live) return;
+    const uint32_t nrows = run.nrows;
+    const uint64_t out_pitch = run.out_pitch, max_n = run.max_n;
+    const int kind = run.kind;
+    const void* work = run.work;
+    const std::vector<uint32_t>& active = run.active;
+    PGB_CUDA(cudaStreamWaitEvent(st, ctx->ev_rms[slot], 0));
 
     // 5. boxcar ladder + runs (re-run with larger buffers on overflow)
     ChainParams cp{};
@@ -409,9 +466,9 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
         ctx->cands_raw.reserve(ctx->cand_cap * sizeof(pgb_candidate));
         ctx->frags.reserve(ctx->frag_cap * sizeof(Fragment));
         PGB_CUDA(cudaMemsetAsync(dcnt, 0, 2 * sizeof(unsigned long long), st));
-        launch_boxcar_peaks(work, kind, ctx->d_row_len.as<uint32_t>(), ctx->frms.as<float>(),
-                            ctx->status.as<uint8_t>(), nrows, out_pitch, max_n, cp,
-                            ctx->d_active.as<uint32_t>(), ctx->d_dms.as<double>(),
+        launch_boxcar_peaks(work, kind, ctx->d_row_len[slot].as<uint32_t>(), ctx->frms[slot].as<float>(),
+                            ctx->status[slot].as<uint8_t>(), nrows, out_pitch, max_n, cp,
+                            ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
                             ctx->d_scale.as<double>(), ctx->cands_raw.as<pgb_candidate>(), dcnt,
                             ctx->cand_cap, ctx->frags.as<Fragment>(), dcnt + 1, ctx->frag_cap, st);
         PGB_CUDA(cudaMemcpyAsync(hcnt, dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
@@ -433,8 +490,8 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
                            ctx->sort_tmp.p, tmp, ctx->sort_keys.as<uint64_t>(),
                            ctx->sort_keys.as<uint64_t>() + nf, ctx->sort_idx.as<uint32_t>(),
                            ctx->sort_idx.as<uint32_t>() + nf, st);
-            launch_stitch(ctx->frags_sorted.as<Fragment>(), nf, ctx->d_row_len.as<uint32_t>(), cp,
-                          ctx->d_active.as<uint32_t>(), ctx->d_dms.as<double>(),
+            launch_stitch(ctx->frags_sorted.as<Fragment>(), nf, ctx->d_row_len[slot].as<uint32_t>(), cp,
+                          ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
                           ctx->cands_raw.as<pgb_candidate>(), dcnt, ctx->cand_cap, st);
             PGB_CUDA(cudaMemcpyAsync(hcnt, dcnt, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
             PGB_CUDA(cudaStreamSynchronize(st));
@@ -463,18 +520,26 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
     }
     // 7. degenerate trials (src/engine.cpp:189-194) join the uncoverable ones
     std::vector<uint8_t> stat(nrows);
-    PGB_CUDA(cudaMemcpyAsync(stat.data(), ctx->status.p, nrows, cudaMemcpyDeviceToHost, st));
+    PGB_CUDA(cudaMemcpyAsync(stat.data(), ctx->status[slot].p, nrows, cudaMemcpyDeviceToHost, st));
     PGB_CUDA(cudaStreamSynchronize(st));
     for (uint32_t r = 0; r < nrows; ++r)
         if (stat[r]) ctx->skipped.push_back(active[r]);
     std::sort(ctx->skipped.begin(), ctx->skipped.end());
     float ms = 0.f;
-    PGB_CUDA(cudaEventElapsedTime(&ms, ctx->ev_dd0, ctx->ev_dd1));
+    PGB_CUDA(cudaEventElapsedTime(&ms, ctx->ev_dd0[slot], ctx->ev_dd1[slot]));
     ctx->dedisp_ms += ms;
     ctx->last_out_pitch = out_pitch;
     ctx->last_nrows = nrows;
-    ctx->last_had_baseline = baseline;
-    ctx->last_u8 = u8;
+    ctx->last_had_baseline = run.baseline;
+    ctx->last_u8 = run.u8;
+}
+
+// Runs the whole chain for one chunk whose samples are already on the device.
+void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spec,
+               const pgb_engine_config* cfg) {
+    ChunkRun run;
+    chunk_front(ctx, in, spec, cfg, 0, run);
+    chunk_back(ctx, run);
 }
 
 // A float chunk whose cells are all integers in [0, 255] (read_chunk's widening of
@@ -596,8 +661,13 @@ pgb_status pgb_create(int device, pgb_context** out) {
         PGB_CUDA(cudaSetDevice(device));
         PGB_CUDA(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
         PGB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
-        PGB_CUDA(cudaEventCreate(&ctx->ev_dd0));
-        PGB_CUDA(cudaEventCreate(&ctx->ev_dd1));
+        PGB_CUDA(cudaStreamCreateWithFlags(&ctx->rms_st, cudaStreamNonBlocking));
+        for (int k = 0; k < 2; ++k) {
+            PGB_CUDA(cudaEventCreate(&ctx->ev_dd0[k]));
+            PGB_CUDA(cudaEventCreate(&ctx->ev_dd1[k]));
+            PGB_CUDA(cudaEventCreateWithFlags(&ctx->ev_front[k], cudaEventDisableTiming));
+            PGB_CUDA(cudaEventCreateWithFlags(&ctx->ev_rms[k], cudaEventDisableTiming));
+        }
         *out = ctx;
     });
 }
@@ -608,9 +678,13 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         cudaSetDevice(ctx->device);
         cudaStreamSynchronize(ctx->st);
         cudaStreamSynchronize(ctx->copy_st);
+        cudaStreamSynchronize(ctx->rms_st);
+        for (int k = 0; k < 2; ++k)
+            for (DevBuf* b : {&ctx->base[k], &ctx->frms[k], &ctx->status[k], &ctx->d_row_len[k],
+                              &ctx->slot_active[k]})
+                b->release();
         for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,
-                          &ctx->base, &ctx->frms, &ctx->status, &ctx->d_active, &ctx->d_row_len,
-                          &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->ws_base, &ctx->ws_off, &ctx->dd_win, &ctx->dd_off, &ctx->rfi_out, &ctx->rfi.chan_bad,
+                          &ctx->d_active, &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->ws_base, &ctx->ws_off, &ctx->dd_win, &ctx->dd_off, &ctx->rfi_out, &ctx->rfi.chan_bad,
                           &ctx->rfi.samp_bad, &ctx->rfi.dbl, &ctx->rfi.tmp, &ctx->rfi.rows, &ctx->cands_raw, &ctx->cands_sorted,
                           &ctx->frags, &ctx->frags_sorted, &ctx->counters, &ctx->sort_keys,
                           &ctx->sort_idx, &ctx->sort_tmp, &ctx->payload, &ctx->file_cands,
@@ -618,8 +692,10 @@ pgb_status pgb_destroy(pgb_context* ctx) {
             b->release();
         ctx->h_counters.release();
         for (auto e : ctx->seg_events) cudaEventDestroy(e);
-        cudaEventDestroy(ctx->ev_dd0);
-        cudaEventDestroy(ctx->ev_dd1);
+        for (int k = 0; k < 2; ++k)
+            for (cudaEvent_t e : {ctx->ev_dd0[k], ctx->ev_dd1[k], ctx->ev_front[k], ctx->ev_rms[k]})
+                cudaEventDestroy(e);
+        cudaStreamDestroy(ctx->rms_st);
         cudaStreamDestroy(ctx->st);
         cudaStreamDestroy(ctx->copy_st);
         delete ctx;
@@ -921,22 +997,9 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
         }
         ctx->file_skipped.clear();
         uint64_t total = 0;
-        std::vector<uint64_t> counts(nchunks);
-        // accumulate per-chunk sorted candidates on the device
-        for (size_t k = 0; k < nchunks; ++k) {
-            validate_cfg(ctx, &chunks[k], cfg);
-            if (!payload_on_device) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
-            const uint8_t* cptr = dpay + chunks[k].start_sample * C;
-            ChunkInput ci{cptr, true};
-            if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
-                uint64_t nbc = 0, nbs = 0;
-                ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);
-                rfi_clean_impl<uint8_t>(cptr, chunks[k].length, C, to_rfi(rfi), ctx->rfi, ctx->rfi_out.as<float>(),
-                                        ctx->st, &nbc, &nbs);
-                ctx->launches += 8;
-                if (nbc || nbs) ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
-            }
-            run_chunk(ctx, ci, &chunks[k], cfg);
+        // back half of a chunk: append its sorted candidates and skipped trials
+        auto finish = [&](ChunkRun& run) {
+            chunk_back(ctx, run);
             const uint64_t nc = ctx->n_cands;
             if (nc) {
                 if ((total + nc) * sizeof(pgb_candidate) > ctx->file_cands.bytes) {
@@ -956,10 +1019,40 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
             }
             total += nc;
             for (uint64_t t : ctx->skipped) {
-                ctx->file_skipped.push_back(chunks[k].index);
+                ctx->file_skipped.push_back(run.spec.index);
                 ctx->file_skipped.push_back(t);
             }
+        };
+        // With a baseline the chain reads the slot's own baseline buffer, so chunk k's
+        // front half (dedispersion + RMS) is issued before chunk k-1's back half: the
+        // RMS of chunk k then runs beside the boxcar of chunk k-1.  Without one the
+        // chain reads the shared series buffer and the halves stay in order.
+        const bool overlap = cfg->baseline_window > 0;
+        ChunkRun runs[2];
+        bool pending = false;
+        for (size_t k = 0; k < nchunks; ++k) {
+            validate_cfg(ctx, &chunks[k], cfg);
+            if (!payload_on_device) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
+            const uint8_t* cptr = dpay + chunks[k].start_sample * C;
+            ChunkInput ci{cptr, true};
+            if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
+                uint64_t nbc = 0, nbs = 0;
+                ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);
+                rfi_clean_impl<uint8_t>(cptr, chunks[k].length, C, to_rfi(rfi), ctx->rfi, ctx->rfi_out.as<float>(),
+                                        ctx->st, &nbc, &nbs);
+                ctx->launches += 8;
+                if (nbc || nbs) ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
+            }
+            ChunkRun& cur = runs[k & 1];
+            chunk_front(ctx, ci, &chunks[k], cfg, (int)(k & 1), cur);
+            if (pending) finish(runs[(k - 1) & 1]);
+            pending = true;
+            if (!overlap) {
+                finish(cur);
+                pending = false;
+            }
         }
+        if (pending) finish(runs[(nchunks - 1) & 1]);
         // file-level sort (src/pipeline.cpp:100-105) and link_grid (:106)
         ctx->file_sorted.reserve(std::max<uint64_t>(total, 1) * sizeof(pgb_candidate));
         if (total) {

@@ -179,14 +179,14 @@ __device__ __forceinline__ float load_x(const void* base, size_t idx) {
 
 // One warp = 8 trials x 4 chains.  The chains are strictly sequential (the
 // reference's rounding order), so the kernel's job is to keep each chain's DADD
-// dependency fed: the 8 rows stream through a 4-stage cp.async ring in shared
+// dependency fed: the 8 rows stream through a 3-stage cp.async ring in shared
 // memory (rows padded by 4 floats so the 32 lanes hit 32 banks), and each lane
 // reads 16 values ahead of its add chain.  Both passes (sum of squares, then the
 // 3-sigma-clipped sum) run in the same kernel.
 constexpr int RMS_TR = 8;          // trials per block
-constexpr int RMS_T = 1024;        // elements per trial per stage
+constexpr int RMS_T = 512;         // elements per trial per stage
 constexpr int RMS_LD = RMS_T + 4;  // padded row length (floats)
-constexpr int RMS_NST = 4;         // ring stages
+constexpr int RMS_NST = 3;         // ring stages (49.5 KB: fits beside a boxcar CTA)
 
 template <int KIND>
 __global__ void __launch_bounds__(32)
