@@ -117,7 +117,11 @@ struct pgb_context {
     // (transpose, dedispersion, baseline, RMS) to its back half (boxcar, runs, order)
     DevBuf base[2], frms[2], status[2], d_row_len[2], slot_active[2];
     DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
-    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off;
+    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off, d_keep;
+    // what the series buffer holds: the dedispersed rows of the raw-sample chunk
+    // [ser_start, ser_start + ser_len) at pitch ser_pitch (overlap reuse)
+    bool ser_ok = false;
+    uint64_t ser_start = 0, ser_len = 0, ser_pitch = 0;
     uint32_t dd_tab_wmax = 0;  // wmax the staging table was built for (0 = stale)
     DevBuf file_cands, file_sorted;
     DevBuf cl_scratch, clusters, members;
@@ -174,6 +178,8 @@ void need(bool cond, pgb_status code, const char* msg) {
 struct ChunkInput {
     const void* data;   // device pointer, time-major
     bool u8;
+    bool raw = false;         // the file's unmodified 8-bit samples (overlap reuse allowed)
+    uint64_t pitch_min = 0;   // series pitch floor (a file search keeps one pitch for all chunks)
 };
 
 // Validation and in-flight arithmetic of run_dm_loop (src/engine.cpp:60-97).
@@ -241,6 +247,10 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         else active.push_back(t);
     }
     const uint32_t nrows = (uint32_t)active.size();
+    // the series buffer holds the previous chunk's rows only if it ran on the same
+    // active set from the file's raw samples (set again below once this chunk is issued)
+    const bool ser_prev = ctx->ser_ok && ctx->geom_valid && ctx->active == active;
+    ctx->ser_ok = false;
     if (nrows == 0) return;
     if (ctx->nchans > 0 && nrows > (1u << 20)) raise(PGB_ERR_CONFIG, "more than 2^20 trials");
 
@@ -309,7 +319,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         }
     }
     const uint32_t ntiles = (uint32_t)((max_n + DD_NT - 1) / DD_NT);
-    const uint64_t out_pitch = (uint64_t)ntiles * DD_NT;
+    const uint64_t out_pitch = std::max<uint64_t>((uint64_t)ntiles * DD_NT, round_up(in.pitch_min, DD_NT));
     const uint64_t rows_pitch =
         round_up((uint64_t)ntiles * DD_NT + maxd_active + std::max(wmax, ws_wmax) + 64, 64);
     const size_t esz = u8 ? 1 : 4;
@@ -365,6 +375,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     dl.wmax = wmax;
     dl.ntiles = ntiles;
     dl.mul24 = 1u << 24;
+    uint64_t reused = 0;  // channel-adds taken over from the previous chunk
     PGB_CUDA(cudaEventRecord(ctx->ev_dd0[slot], st));
     if (u8 && ws_g) {
         DedispLaunch dw = dl;
@@ -389,7 +400,45 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         }
         dl.dd_win = ctx->dd_win.as<uint2>();
         dl.dd_off = ctx->dd_off.as<uint32_t>();
+        // Overlap reuse (file search, raw 8-bit chunks): the dedispersed value of an
+        // absolute sample does not depend on the chunk, so outputs chunk k-1 already
+        // produced -- [start_k, start_{k-1} + L_{k-1} - d_t) for trial t -- are moved to
+        // the front of each row instead of being summed again.  Every output of chunk k
+        // is still a sum over the same input bytes, so the series is unchanged bit for bit.
+        if (in.raw && ser_prev && out_pitch == ctx->ser_pitch && spec->start_sample > ctx->ser_start &&
+            !getenv("PGB_NO_OVERLAP_REUSE")) {
+            const uint64_t shift = spec->start_sample - ctx->ser_start;
+            std::vector<uint32_t> keep(nrows);
+            uint64_t kmax = 0;
+            for (uint32_t r = 0; r < nrows; ++r) {
+                const uint64_t prev_n = ctx->ser_len - (uint64_t)ctx->maxd[active[r]];
+                const uint64_t k = prev_n > shift ? std::min<uint64_t>(prev_n - shift, row_len[r]) : 0;
+                keep[r] = (uint32_t)k;
+                kmax = std::max(kmax, k);
+            }
+            if (kmax >= DD_NT && shift >= kmax) {
+                std::vector<uint32_t> first(nblocks, UINT32_MAX);
+                for (uint32_t r = 0; r < nrows; ++r)
+                    first[r / tb] = std::min<uint32_t>(first[r / tb], keep[r] / DD_NT);
+                const uint32_t tile0 = *std::min_element(first.begin(), first.end());
+                ctx->d_keep.reserve((size_t)(nrows + nblocks) * sizeof(uint32_t));
+                uint32_t* dk = ctx->d_keep.as<uint32_t>();
+                PGB_CUDA(cudaMemcpyAsync(dk, keep.data(), nrows * 4, cudaMemcpyHostToDevice, st));
+                PGB_CUDA(cudaMemcpyAsync(dk + nrows, first.data(), nblocks * 4, cudaMemcpyHostToDevice, st));
+                launch_series_shift(ctx->series.as<int32_t>(), nrows, out_pitch, shift, dk, st);
+                ctx->launches += 1;
+                dl.blk_first = dk + nrows;
+                dl.tile0 = tile0;
+                for (uint32_t r = 0; r < nrows; ++r) reused += (uint64_t)keep[r] * C;
+            }
+        }
         launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+        if (in.raw) {
+            ctx->ser_ok = true;
+            ctx->ser_start = spec->start_sample;
+            ctx->ser_len = L;
+            ctx->ser_pitch = out_pitch;
+        }
     }
     else launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
     PGB_CUDA(cudaEventRecord(ctx->ev_dd1[slot], st));
@@ -397,7 +446,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     ctx->launches += 2;
     uint64_t adds = 0;
     for (uint32_t r = 0; r < nrows; ++r) adds += (uint64_t)row_len[r] * C;
-    ctx->channel_adds += adds;
+    ctx->channel_adds += adds - reused;
 
     // 3. baseline, 4. robust RMS (on rms_st: one sequential chain per thread, so it
     // leaves the SMs nearly idle and overlaps the previous chunk's boxcar)
@@ -1028,6 +1077,9 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
         // RMS of chunk k then runs beside the boxcar of chunk k-1.  Without one the
         // chain reads the shared series buffer and the halves stay in order.
         const bool overlap = cfg->baseline_window > 0;
+        uint64_t pitch_min = 0;  // one series pitch for the whole file (overlap reuse)
+        for (size_t k = 0; k < nchunks; ++k) pitch_min = std::max<uint64_t>(pitch_min, chunks[k].length);
+        ctx->ser_ok = false;
         ChunkRun runs[2];
         bool pending = false;
         for (size_t k = 0; k < nchunks; ++k) {
@@ -1035,13 +1087,18 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
             if (!payload_on_device) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
             const uint8_t* cptr = dpay + chunks[k].start_sample * C;
             ChunkInput ci{cptr, true};
+            ci.raw = true;
+            ci.pitch_min = pitch_min;
             if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
                 uint64_t nbc = 0, nbs = 0;
                 ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);
                 rfi_clean_impl<uint8_t>(cptr, chunks[k].length, C, to_rfi(rfi), ctx->rfi, ctx->rfi_out.as<float>(),
                                         ctx->st, &nbc, &nbs);
                 ctx->launches += 8;
-                if (nbc || nbs) ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
+                if (nbc || nbs) {
+                    ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
+                    ci.pitch_min = pitch_min;
+                }
             }
             ChunkRun& cur = runs[k & 1];
             chunk_front(ctx, ci, &chunks[k], cfg, (int)(k & 1), cur);

@@ -107,7 +107,9 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     const uint32_t blk = blockIdx.x;
     const uint32_t row0 = blk * TB;
     const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
-    const uint64_t i0 = (uint64_t)blockIdx.y * DD_NT;
+    const uint32_t tile = blockIdx.y + p.tile0;
+    if (p.blk_first && tile < p.blk_first[blk]) return;  // shifted in from the previous chunk
+    const uint64_t i0 = (uint64_t)tile * DD_NT;
     if (i0 >= blk_len[blk]) return;  // every trial of the block is shorter than this tile
     if (threadIdx.x < 32)
         trial_ids[threadIdx.x] = p.active[row0 + min((uint32_t)threadIdx.x, nrows_blk - 1)];
@@ -313,7 +315,9 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     const uint32_t blk = blockIdx.x;
     const uint32_t row0 = blk * TB;
     const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
-    const uint64_t i0 = (uint64_t)blockIdx.y * DD_NT;
+    const uint32_t tile = blockIdx.y + p.tile0;
+    if (p.blk_first && tile < p.blk_first[blk]) return;  // shifted in from the previous chunk
+    const uint64_t i0 = (uint64_t)tile * DD_NT;
     if (i0 >= blk_len[blk]) return;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -553,6 +557,16 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     }
 }
 
+// Overlap reuse: chunk k's first keep[r] outputs of row r are chunk k-1's outputs
+// [shift, shift + keep[r]) (same absolute samples, same input bytes), moved in place.
+__global__ void series_shift_kernel(int32_t* __restrict__ series, uint64_t pitch, uint64_t shift,
+                                    const uint32_t* __restrict__ keep) {
+    int32_t* row = series + (size_t)blockIdx.y * pitch;
+    const uint32_t n = keep[blockIdx.y];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+        row[i] = row[shift + i];
+}
+
 // ---- transposes ---------------------------------------------------------------
 
 // u8 [length][nchans] -> rows [nchans][pitch]; 64x64-byte tiles.
@@ -651,7 +665,7 @@ size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax) {
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
     const size_t smem = dedisp_smem_bytes(true, p.g, p.wmax);
     const int tb = DD_WARPS * p.tpw;
-    dim3 grid((p.nrows + tb - 1) / tb, p.ntiles);
+    dim3 grid((p.nrows + tb - 1) / tb, p.ntiles - p.tile0);
     static const int mode = [] {
         const char* e = getenv("PGB_DD_HMODE");
         return e ? atoi(e) : 3;
@@ -722,6 +736,13 @@ void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cud
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         dedisp_f32_kernel<1><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);
     }
+    PGB_CUDA(cudaGetLastError());
+}
+
+void launch_series_shift(int32_t* series, uint32_t nrows, uint64_t pitch, uint64_t shift,
+                         const uint32_t* keep, cudaStream_t st) {
+    if (!nrows) return;
+    series_shift_kernel<<<dim3(8, nrows), 512, 0, st>>>(series, pitch, shift, keep);
     PGB_CUDA(cudaGetLastError());
 }
 

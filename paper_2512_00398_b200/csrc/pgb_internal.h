@@ -114,11 +114,18 @@ struct DedispLaunch {
     // per (block, channel, trial) byte offset into the 4-copy staging layout
     const uint2* dd_win;        // [nblocks][nchans_pad] {delay min & ~15, 16-byte vectors}
     const uint32_t* dd_off;     // [nblocks][nchans_pad][32]
+    // overlap reuse (file search): tiles below blk_first[block] already hold this
+    // chunk's series (shifted in from the previous chunk); grid.y starts at tile0
+    const uint32_t* blk_first;  // [nblocks] or null
+    uint32_t tile0;
 };
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st);
 // builds p.dd_win / p.dd_off for the active set (tile independent; p.wmax = bytes per copy)
 void launch_dd_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st);
 void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st);
+// series[r][i] = series[r][shift + i] for i < keep[r] (disjoint: shift >= keep[r])
+void launch_series_shift(int32_t* series, uint32_t nrows, uint64_t pitch, uint64_t shift,
+                         const uint32_t* keep, cudaStream_t st);
 size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax);
 // warp-specialized TMA variant (dedisp_tma.cu); p.wmax (bytes) must be a multiple of 256
 void launch_dedisp_u8_ws(const DedispLaunch& p, int nslot, const uint8_t* rows, int32_t* out,

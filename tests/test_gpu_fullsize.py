@@ -80,3 +80,23 @@ def test_config_b_whole_file_recovers_pulses(engine):
                    (np.abs(rep["peak_sample"].astype(np.int64) - t0) <= width + 8)]
         assert len(near) > 0, (trial, t0, width, snr)
     assert checked >= 5
+
+
+def test_config_b_overlap_reuse_is_exact(engine, monkeypatch):
+    """search_file moves the outputs chunk k-1 already dedispersed into chunk k instead of
+    summing them again; the candidate list must equal the recompute-everything run."""
+    import bench
+
+    cfg = dict(bench.CONFIG_B)
+    task = bench.build_task(cfg)
+    payload = bench.make_payload(cfg, task.plan)
+    a, ca, _ = engine.search_file(payload, cfg["nsamples"], task.chunks, task.plan, task.engine)
+    _, _, adds_reuse = engine.last_dedisp_time()
+    monkeypatch.setenv("PGB_NO_OVERLAP_REUSE", "1")
+    b, cb, _ = engine.search_file(payload, cfg["nsamples"], task.chunks, task.plan, task.engine)
+    _, _, adds_full = engine.last_dedisp_time()
+    assert adds_reuse < 0.96 * adds_full  # the reuse actually happened
+    assert len(a) == len(b) > 0
+    for k in a.dtype.names:
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(ca.records, cb.records)
