@@ -364,6 +364,15 @@ __device__ void emit_fragment(const PeakCtx& c, uint32_t row, uint32_t level, ui
     c.frags[slot] = f;
 }
 
+// One ladder level whose partner element is H registers further in the same thread
+// (k ascending: r[k + H] is read before it is updated).  Partners past the tile add 0;
+// they only feed outputs beyond the tile's T valid ones.
+template <int S, int H>
+__device__ __forceinline__ void ladder_regs(double (&r)[S]) {
+#pragma unroll
+    for (int k = 0; k < S; ++k) r[k] = __dadd_rn(r[k], k + H < S ? r[k + H] : 0.0);  // :219
+}
+
 template <int KIND, int S>
 __global__ void __launch_bounds__(BX_THREADS)
     boxcar_peaks_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len,
@@ -415,14 +424,40 @@ __global__ void __launch_bounds__(BX_THREADS)
     uint32_t level = 0;
     for (uint64_t w = 1; w <= bmax && w <= n; w <<= 1, ++level) {
         const uint64_t m = n - w + 1;
-        if (w > 1) {
-            const uint32_t half = (uint32_t)(w >> 1);
+        const uint32_t half = (uint32_t)(w >> 1);
+        // half >= BX_THREADS: element j + half = tid + BX_THREADS (k + half / BX_THREADS)
+        // is this thread's own register; the level needs no shared memory (cur is only
+        // refreshed when a scan needs it)
+        const bool in_regs = half >= (uint32_t)BX_THREADS;
+        if (in_regs) {
+            switch (half / BX_THREADS) {
+                case 1: ladder_regs<S, 1>(r); break;
+                case 2: ladder_regs<S, 2>(r); break;
+                case 4: ladder_regs<S, 4>(r); break;
+                case 8: ladder_regs<S, 8>(r); break;
+                default: ladder_regs<S, S>(r); break;  // beyond the tile: adds zeros
+            }
+        } else if (w > 1) {
+            // cur and nxt are distinct buffers: read a batch of shifted values before
+            // storing any of them, so the LDS latencies overlap instead of serialising
+            // behind the stores the compiler cannot prove independent
+            const double* __restrict__ src = cur;
+            double* __restrict__ dst = nxt;
+            constexpr int HB = 8;
 #pragma unroll
-            for (int k = 0; k < S; ++k) {
-                const uint32_t j = tid + BX_THREADS * k;
-                const double sh = (kPad || j + half < N) ? cur[j + half] : 0.0;
-                r[k] = __dadd_rn(r[k], sh);  // :219
-                nxt[j] = r[k];
+            for (int k0 = 0; k0 < S; k0 += HB) {
+                double sh[HB];
+#pragma unroll
+                for (int q = 0; q < HB; ++q) {
+                    const uint32_t j = tid + BX_THREADS * (k0 + q);
+                    sh[q] = (kPad || j + half < N) ? src[j + half] : 0.0;
+                }
+#pragma unroll
+                for (int q = 0; q < HB; ++q) {
+                    const uint32_t j = tid + BX_THREADS * (k0 + q);
+                    r[k0 + q] = __dadd_rn(r[k0 + q], sh[q]);  // :219
+                    dst[j] = r[k0 + q];
+                }
             }
             double* t = cur;
             cur = nxt;
@@ -437,6 +472,11 @@ __global__ void __launch_bounds__(BX_THREADS)
             any |= (j < lim2) & (__dmul_rn(r[k], sc) > thr);
         }
         if (__syncthreads_or(any)) {
+            if (in_regs) {  // publish the register level for the strip scan
+#pragma unroll
+                for (int k = 0; k < S; ++k) cur[tid + BX_THREADS * k] = r[k];
+                __syncthreads();
+            }
             // contiguous strip scan: thread owns [tid*S, tid*S + S) of the tile
             const uint32_t lo = (uint32_t)tid * S;
             const uint32_t hi = min(lo + S, lim2);
@@ -541,7 +581,9 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
     if (!nrows || !max_len) return;
     PeakCtx ctx{active, dms, cp, cands, n_cands, cand_cap, frags, n_frags, frag_cap};
     const uint64_t bmax = cp.boxcar_max;
-    const int S = bmax <= 4096 ? 16 : 24;  // 2 x N doubles must fit in 227 KB
+    // 2 x N doubles must fit in 227 KB.  A tile yields N - bmax outputs, so for the
+    // long ladders S = 24 (N = 12288, 1.5x halo overhead instead of 2x at bmax 4096)
+    const int S = bmax <= 2048 ? 16 : 24;
     const uint64_t N = (uint64_t)BX_THREADS * S;
     const uint64_t LD = S == 16 ? N + N / 4 : N;
     const uint64_t T = N - bmax;

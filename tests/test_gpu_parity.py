@@ -87,6 +87,25 @@ def test_run_dm_loop_u8_vs_port(engine, port, window, bmax):
     assert np.array_equal(res.skipped_trials, want_sk)
 
 
+@pytest.mark.parametrize("bmax", [2048, 4096])
+def test_run_dm_loop_runs_across_boxcar_tiles(engine, port, bmax):
+    """Wide and narrow pulses straddling the boxcar tile boundaries (8192 outputs per
+    tile at bmax 4096, 6144 at 2048): runs split into fragments must stitch back."""
+    hdr = FilterbankHeader(fch1=1500.0, foff=-1.0, nchans=128, tsamp=64e-6)
+    plan = generate_dm_trials(0.0, 60.0, hdr, LinearSpacing(4.0))
+    L = 40000
+    T = 8192 if bmax == 4096 else 6144
+    data = u8_chunk(hdr, plan, L, seed=21, pulses=[(3, T - 40, 128, 30.0), (9, 2 * T - 3, 8, 25.0),
+                                                   (12, 3 * T - 700, 1024, 40.0)])
+    cfg = EngineConfig(n_workers=1, tsamp=hdr.tsamp, boxcar_max=bmax, baseline_window=8001)
+    spec = ChunkSpec.whole(L)
+    res = engine.run_dm_loop(Chunk(spec, data), plan, cfg)
+    want, want_sk = port.run_dm_loop(data, vars(spec), plan.dms, plan.delays, cfg_dict(cfg))
+    assert len(want) > 0
+    assert_same_candidates(res.candidates, want)
+    assert np.array_equal(res.skipped_trials, want_sk)
+
+
 def test_run_dm_loop_u8_chunk_edges(engine, ref):
     """Interior chunk of a file: start > 0, overlap > 0, valid range < chunk
     (edge-run drops and valid-range filter, src/detect.cpp:235-238)."""
