@@ -363,7 +363,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 #pragma unroll
                 for (int s = 1; s < 4; ++s) {
                     uint4 sh;
-                    if (SF) {  // funnel shift on the FMA pipe: (lo >> 8s) + hi * 2^(32-8s)
+                    if (SF & 1) {  // funnel shift on the FMA pipe: (lo >> 8s) + hi * 2^(32-8s)
                         const uint32_t k = kshift[s - 1];
                         uint32_t q[4];
 #pragma unroll
@@ -457,7 +457,13 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
                     uint32_t e = E[u][m];
                     asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(e) : "r"(w & 0x00ff00ffu), "r"(one));
                     E[u][m] = e;
-                    H[u][m] += __umulhi(w, 1u << 24);
+                    if ((SF & 2) && (m & 1)) {  // odd words: H on the FMA pipe (IMAD.HI)
+                        uint32_t h = H[u][m];
+                        asm("mad.hi.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(w), "r"(kshift[0]));
+                        H[u][m] = h;
+                    } else {
+                        H[u][m] += __umulhi(w, 1u << 24);  // LEA.HI, ALU pipe
+                    }
                 }
             }
         }
@@ -674,9 +680,11 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const char* e = getenv("PGB_DD_V1");
         return e && *e && *e != '0';
     }();
-    static const int sf = [] {  // PGB_DD_SFMA=1: staging shifts on the FMA pipe (ablation)
+    static const int sf = [] {  // variant bits: 1 = staging shifts on the FMA pipe (ablation),
+        // 2 = odd-word H accumulation on the FMA pipe (IMAD.HI) to balance ALU/FMA
         const char* e = getenv("PGB_DD_SFMA");
-        return e && *e == '1' ? 1 : 0;
+        const char* h = getenv("PGB_DD_HHI");
+        return (e && *e == '1' ? 1 : 0) | (h && *h == '1' ? 2 : 0);
     }();
     if (!v1 && p.tpw == 2 && p.dd_off) {
         // vectors per staging thread: ceil(max window vectors / (32 * warps per channel))
@@ -691,6 +699,7 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         return;                                                                                   \
     }
 #define PGB_TAB(G_, V_) PGB_TAB3(G_, V_, 0) PGB_TAB3(G_, V_, 1)
+        PGB_TAB3(8, 2, 2) PGB_TAB3(8, 2, 3)
         PGB_TAB(8, 1) PGB_TAB(8, 2) PGB_TAB(8, 4)
         PGB_TAB(4, 1) PGB_TAB(4, 2) PGB_TAB(4, 4)
         PGB_TAB(2, 1) PGB_TAB(2, 2) PGB_TAB(2, 4)
