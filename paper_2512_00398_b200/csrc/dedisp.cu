@@ -266,6 +266,223 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     }
 }
 
+// ---- mbarrier ring variant ---------------------------------------------------------
+// Same tile, table, staging layout and SWAR accumulation as dedisp_u8_tab_kernel, but the
+// CTA-wide barrier per stage is replaced by per-slot mbarriers over a 3-slot ring:
+//   iteration g: issue the global loads of stage g+2 -> wait full[g%3] -> add stage g ->
+//   arrive empty[g%3] -> wait empty of stage g-1 (the slot stage g+2 reuses) -> shift and
+//   store stage g+2 -> arrive full[(g+2)%3].
+// A warp only waits for the others to have finished stage g-1, so warps drift up to a
+// stage apart instead of meeting at every stage (the barrier cost ~7 ms of 51 per
+// config-B chunk: timing experiment "no barrier").
+__device__ __forceinline__ uint32_t sh_addr(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void ring_init(uint64_t* bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sh_addr(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void ring_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(sh_addr(bar)) : "memory");
+}
+__device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
+    const uint32_t a = sh_addr(bar);
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+
+constexpr int RING_NS = 3;
+
+template <int G, int VPT>
+__global__ void __launch_bounds__(DD_THREADS, 1)
+    dedisp_u8_ring_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
+                          int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    constexpr int TPW = 2;
+    constexpr int TB = DD_WARPS * TPW;
+    static_assert(TB == 32, "table layout assumes 32-trial blocks");
+    constexpr int NS = RING_NS;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t W = p.wmax;  // bytes per copy
+    uint8_t* buf = smem;                                                           // [NS][G][4][W]
+    uint32_t* offs = reinterpret_cast<uint32_t*>(smem + (size_t)NS * G * 4 * W);  // [NS][G][TB]
+    uint64_t* full = reinterpret_cast<uint64_t*>(offs + NS * G * TB);              // [NS]
+    uint64_t* empty = full + NS;                                                   // [NS]
+
+    const uint32_t blk = blockIdx.x;
+    const uint32_t row0 = blk * TB;
+    const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
+    const uint32_t tile = blockIdx.y + p.tile0;
+    if (p.blk_first && tile < p.blk_first[blk]) return;  // shifted in from the previous chunk
+    const uint64_t i0 = (uint64_t)tile * DD_NT;
+    if (i0 >= blk_len[blk]) return;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t nstages = p.nchans_pad / G;
+    constexpr int wpc = DD_WARPS / G;
+    const int my_cs = warp / wpc;
+    const uint32_t my_t = (uint32_t)((warp % wpc) * 32 + lane);
+    constexpr uint32_t vstride = (uint32_t)wpc * 32;
+    const uint32_t* offtab = p.dd_off + (size_t)blk * p.nchans_pad * TB;
+    const uint2* wintab = p.dd_win + (size_t)blk * p.nchans_pad;
+    const uint8_t* rows_i0 = rows + i0;
+    constexpr bool kOffs = true;
+    const bool offs_thread = (int)threadIdx.x < G * TB / 4;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            ring_init(full + s, DD_WARPS);
+            ring_init(empty + s, DD_WARPS);
+        }
+    }
+    __syncthreads();
+
+    uint4 v0[VPT];
+    uint32_t v1[VPT];
+    uint4 ov = make_uint4(0, 0, 0, 0);
+
+    auto load_stage = [&](uint32_t gi, uint2 wv) {
+        const uint8_t* src = rows_i0 + (size_t)(gi * G + my_cs) * p.rows_pitch + wv.x;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const uint32_t vi = my_t + k * vstride;
+            if (vi < wv.y) {
+                v0[k] = __ldg(reinterpret_cast<const uint4*>(src + 16 * vi));
+                v1[k] = __ldg(reinterpret_cast<const uint32_t*>(src + 16 * vi + 16));
+            }
+        }
+        if (kOffs && offs_thread)
+            ov = __ldg(reinterpret_cast<const uint4*>(offtab + (size_t)gi * G * TB) + threadIdx.x);
+    };
+    auto store_stage = [&](int slot, uint2 wv) {
+        uint8_t* base = buf + (size_t)((slot * G + my_cs) * 4) * W;
+#pragma unroll
+        for (int k = 0; k < VPT; ++k) {
+            const uint32_t vi = my_t + k * vstride;
+            if (vi < wv.y) {
+                uint8_t* dst = base + 16 * vi;
+                const uint32_t w[5] = {v0[k].x, v0[k].y, v0[k].z, v0[k].w, v1[k]};
+                *reinterpret_cast<uint4*>(dst) = v0[k];
+#pragma unroll
+                for (int s = 1; s < 4; ++s) {
+                    const uint32_t sel = (uint32_t)(s | (s + 1) << 4 | (s + 2) << 8 | (s + 3) << 12);
+                    uint4 sh;
+                    sh.x = __byte_perm(w[0], w[1], sel);
+                    sh.y = __byte_perm(w[1], w[2], sel);
+                    sh.z = __byte_perm(w[2], w[3], sel);
+                    sh.w = __byte_perm(w[3], w[4], sel);
+                    *reinterpret_cast<uint4*>(dst + (size_t)s * W) = sh;
+                }
+            }
+        }
+        if (kOffs && offs_thread) reinterpret_cast<uint4*>(offs + slot * G * TB)[threadIdx.x] = ov;
+        __syncwarp();
+        if (lane == 0) ring_arrive(full + slot);
+    };
+
+    uint32_t E[TPW][DD_WORDS], H[TPW][DD_WORDS];
+    const uint32_t one = p.mul24 >> 24;  // 1, opaque to the compiler (keeps E on IMAD)
+#pragma unroll
+    for (int u = 0; u < TPW; ++u)
+#pragma unroll
+        for (int m = 0; m < DD_WORDS; ++m) E[u][m] = H[u][m] = 0;
+    bool first_flush = true;
+
+    auto flush = [&]() {
+#pragma unroll
+        for (int u = 0; u < TPW; ++u) {
+            const uint32_t r = warp * TPW + u;
+            if (r < nrows_blk) {
+                int32_t* dst = out + (size_t)(row0 + r) * p.out_pitch + i0;
+#pragma unroll
+                for (int m = 0; m < DD_WORDS; ++m) {
+                    const uint32_t e = E[u][m];
+                    const uint32_t b0 = e & 0xffffu, b2 = e >> 16;
+                    const uint32_t t = H[u][m] - (b2 << 8);  // B1 + 2^16 B3
+                    int4 val = make_int4((int)b0, (int)(t & 0xffffu), (int)b2, (int)(t >> 16));
+                    int4* pd = reinterpret_cast<int4*>(dst + 4 * (lane + 32 * m));
+                    if (!first_flush) {
+                        const int4 old = *pd;
+                        val.x += old.x;
+                        val.y += old.y;
+                        val.z += old.z;
+                        val.w += old.w;
+                    }
+                    *pd = val;
+                }
+            }
+#pragma unroll
+            for (int m = 0; m < DD_WORDS; ++m) E[u][m] = H[u][m] = 0;
+        }
+        first_flush = false;
+    };
+
+    // prologue: stages 0 and 1 into slots 0 and 1 (full phase 0 of each)
+    {
+        const uint2 w0 = __ldg(wintab + my_cs);
+        load_stage(0, w0);
+        store_stage(0, w0);
+        if (nstages > 1) {
+            const uint2 w1 = __ldg(wintab + G + my_cs);
+            load_stage(1, w1);
+            store_stage(1, w1);
+        }
+    }
+    uint2 wnext = nstages > 2 ? __ldg(wintab + 2 * G + my_cs) : make_uint2(0, 0);
+    const uint32_t stages_per_flush = DD_FLUSH_CH / G;
+    uint32_t since_flush = 0;
+    int slot = 0, slot2 = 2;          // gi % NS, (gi + 2) % NS
+    uint32_t ph = 0, ph_prev = 0;     // parity of stage gi's use of its slot; of stage gi-1's
+
+    for (uint32_t gi = 0; gi < nstages; ++gi) {
+        const bool pre = gi + 2 < nstages;
+        const uint2 wstage = wnext;
+        if (pre) {
+            load_stage(gi + 2, wstage);
+            if (gi + 3 < nstages) wnext = __ldg(wintab + (size_t)(gi + 3) * G + my_cs);
+        }
+        ring_wait(full + slot, ph);
+        const uint32_t* offb = offs + slot * G * TB + warp * TPW;
+        const uint8_t* bufb = buf + (size_t)slot * G * 4 * W + 4 * lane;
+#pragma unroll
+        for (int cs = 0; cs < G; ++cs) {
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                const uint8_t* src = bufb + (size_t)cs * 4 * W + offb[cs * TB + u];
+#pragma unroll
+                for (int m = 0; m < DD_WORDS; ++m) {
+                    const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 128 * m);
+                    uint32_t e = E[u][m];
+                    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(e) : "r"(w & 0x00ff00ffu), "r"(one));
+                    E[u][m] = e;
+                    H[u][m] += __umulhi(w, 1u << 24);  // LEA.HI, ALU pipe
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) ring_arrive(empty + slot);
+        if (pre) {
+            // slot2 last held stage gi-1: every warp must be done adding it
+            if (gi >= 1) ring_wait(empty + slot2, ph_prev);
+            store_stage(slot2, wstage);
+        }
+        if (++since_flush == stages_per_flush || gi + 1 == nstages) {
+            flush();
+            since_flush = 0;
+        }
+        // advance ring indices: stage gi+1 uses slot (gi+1)%NS, use count (gi+1)/NS
+        ph_prev = ph;
+        if (++slot == NS) { slot = 0; ph ^= 1; }
+        if (++slot2 == NS) slot2 = 0;
+    }
+}
+
 // Tile-independent staging geometry of the u8 kernel, one warp per (trial block,
 // channel): the window of channel c for a block starts at i0 + (min_t d_t(c) & ~15)
 // (i0 is a multiple of DD_NT, so 16-byte aligned) and trial t reads it at
@@ -304,6 +521,9 @@ template <int G, int VPT, int SF>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_u8_tab_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
                          int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    // timing experiments (builds with -DPGB_DD_EXPERIMENTS only; results are wrong):
+    // 4 = no adds, 8 = no staging, 16 = no flush, 32 = no barrier
+    constexpr int XP = SF & ~3;
     constexpr int TPW = 2;
     constexpr int TB = DD_WARPS * TPW;
     static_assert(TB == 32, "table layout assumes 32-trial blocks");
@@ -441,13 +661,13 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
         const uint2 wstage = wnext;
         if (more) {
             fetch_offs(gi + 1, b ^ 1);
-            load_stage(gi + 1, wstage);
+            if (!(XP & 8)) load_stage(gi + 1, wstage);
             if (gi + 2 < nstages) wnext = __ldg(wintab + (size_t)(gi + 2) * G + my_cs);
         }
         const uint32_t* offb = offs + b * G * TB + warp * TPW;
         const uint8_t* bufb = buf + (size_t)b * G * 4 * W + 4 * lane;
 #pragma unroll
-        for (int cs = 0; cs < G; ++cs) {
+        for (int cs = 0; cs < ((XP & 4) ? 0 : G); ++cs) {
 #pragma unroll
             for (int u = 0; u < TPW; ++u) {
                 const uint8_t* src = bufb + (size_t)cs * 4 * W + offb[cs * TB + u];
@@ -467,13 +687,13 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
                 }
             }
         }
-        if (more) store_stage(b ^ 1, wstage);
+        if (more && !(XP & 8)) store_stage(b ^ 1, wstage);
         if (++since_flush == stages_per_flush || !more) {
-            flush();
+            if (!(XP & 16)) flush();
             since_flush = 0;
         }
         __pipeline_wait_prior(0);
-        __syncthreads();
+        if (!(XP & 32)) __syncthreads();
     }
 }
 
@@ -668,6 +888,10 @@ size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax) {
     return staged + (size_t)2 * g * tb * 4 + (size_t)2 * g * 8;
 }
 
+size_t ring_smem_bytes(int g, uint32_t wmax) {
+    return (size_t)RING_NS * g * 4 * wmax + (size_t)RING_NS * g * 32 * 4 + 2 * RING_NS * sizeof(uint64_t);
+}
+
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
     const size_t smem = dedisp_smem_bytes(true, p.g, p.wmax);
     const int tb = DD_WARPS * p.tpw;
@@ -684,8 +908,38 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         // 2 = odd-word H accumulation on the FMA pipe (IMAD.HI) to balance ALU/FMA
         const char* e = getenv("PGB_DD_SFMA");
         const char* h = getenv("PGB_DD_HHI");
-        return (e && *e == '1' ? 1 : 0) | (h && *h == '1' ? 2 : 0);
+        int v = (e && *e == '1' ? 1 : 0) | (h && *h == '1' ? 2 : 0);
+#ifdef PGB_DD_EXPERIMENTS
+        if (const char* x = getenv("PGB_DD_EXPERIMENT")) v |= atoi(x) & ~3;
+#endif
+        return v;
     }();
+    static const bool ring = [] {  // PGB_DD_RING=0: CTA-barrier kernel instead of the mbarrier ring
+        const char* e = getenv("PGB_DD_RING");
+        return !(e && *e == '0');
+    }();
+    if (ring && !v1 && !sf && p.tpw == 2 && p.dd_off) {
+        int g = 8;
+        while (g > 1 && ring_smem_bytes(g, p.wmax) > 227 * 1024) g >>= 1;
+        const size_t rsm = ring_smem_bytes(g, p.wmax);
+        const uint32_t vstride = 32u * (DD_WARPS / g);
+        const int vpt = (int)((p.wmax / 16 + vstride - 1) / vstride);
+        if (rsm <= 227 * 1024) {
+#define PGB_RING(G_, V_)                                                                          \
+    if (g == G_ && vpt <= V_) {                                                                   \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_kernel<G_, V_>,                              \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \
+        dedisp_u8_ring_kernel<G_, V_><<<grid, DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len);    \
+        PGB_CUDA(cudaGetLastError());                                                             \
+        return;                                                                                   \
+    }
+            PGB_RING(8, 1) PGB_RING(8, 2) PGB_RING(8, 4)
+            PGB_RING(4, 1) PGB_RING(4, 2) PGB_RING(4, 4)
+            PGB_RING(2, 1) PGB_RING(2, 2) PGB_RING(2, 4)
+            PGB_RING(1, 1) PGB_RING(1, 2) PGB_RING(1, 4)
+#undef PGB_RING
+        }
+    }
     if (!v1 && p.tpw == 2 && p.dd_off) {
         // vectors per staging thread: ceil(max window vectors / (32 * warps per channel))
         const uint32_t vstride = 32u * (DD_WARPS / p.g);
@@ -700,6 +954,10 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
     }
 #define PGB_TAB(G_, V_) PGB_TAB3(G_, V_, 0) PGB_TAB3(G_, V_, 1)
         PGB_TAB3(8, 2, 2) PGB_TAB3(8, 2, 3)
+#ifdef PGB_DD_EXPERIMENTS
+        PGB_TAB3(8, 2, 4) PGB_TAB3(8, 2, 8) PGB_TAB3(8, 2, 40) PGB_TAB3(8, 2, 24) PGB_TAB3(8, 2, 56)
+        PGB_TAB3(8, 2, 32) PGB_TAB3(8, 2, 16) PGB_TAB3(8, 2, 48)
+#endif
         PGB_TAB(8, 1) PGB_TAB(8, 2) PGB_TAB(8, 4)
         PGB_TAB(4, 1) PGB_TAB(4, 2) PGB_TAB(4, 4)
         PGB_TAB(2, 1) PGB_TAB(2, 2) PGB_TAB(2, 4)
