@@ -464,11 +464,13 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         work = ctx->base[slot].p;
         kind = 0;
     }
+    static const bool rms_main = getenv("PGB_RMS_MAIN") != nullptr;  // experiment: no overlap
+    cudaStream_t rst = rms_main ? st : ctx->rms_st;
     PGB_CUDA(cudaEventRecord(ctx->ev_front[slot], st));
-    PGB_CUDA(cudaStreamWaitEvent(ctx->rms_st, ctx->ev_front[slot], 0));
+    PGB_CUDA(cudaStreamWaitEvent(rst, ctx->ev_front[slot], 0));
     launch_rms(work, kind, d_len, nrows, out_pitch, ctx->frms[slot].as<float>(),
-               ctx->status[slot].as<uint8_t>(), ctx->rms_st);
-    PGB_CUDA(cudaEventRecord(ctx->ev_rms[slot], ctx->rms_st));
+               ctx->status[slot].as<uint8_t>(), rst);
+    PGB_CUDA(cudaEventRecord(ctx->ev_rms[slot], rst));
     ctx->launches += 5;
 
     run.live = true;

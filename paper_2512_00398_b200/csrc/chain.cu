@@ -183,18 +183,25 @@ __device__ __forceinline__ float load_x(const void* base, size_t idx) {
 // memory (rows padded by 4 floats so the 32 lanes hit 32 banks), and each lane
 // reads 16 values ahead of its add chain.  Both passes (sum of squares, then the
 // 3-sigma-clipped sum) run in the same kernel.
-constexpr int RMS_TR = 8;          // trials per block
-constexpr int RMS_T = 512;         // elements per trial per stage
+constexpr int RMS_TR = 8;          // trials per warp
+constexpr int RMS_T = 128;         // elements per trial per stage
 constexpr int RMS_LD = RMS_T + 4;  // padded row length (floats)
-constexpr int RMS_NST = 3;         // ring stages (49.5 KB: fits beside a boxcar CTA)
+constexpr int RMS_NST = 3;         // ring stages per warp
+// 16 warps (128 trials) per block: the chains are latency-bound, so packing them onto
+// few SMs (8 for 1001 trials) costs the concurrently running dedispersion/boxcar
+// kernels 8 SMs instead of one SM per 8 trials
+constexpr int RMS_WARPS = 16;
 
 template <int KIND>
-__global__ void __launch_bounds__(32)
+__global__ void __launch_bounds__(32 * RMS_WARPS)
     rms_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len, uint32_t nrows,
                uint64_t pitch, float* __restrict__ frms, uint8_t* __restrict__ status) {
-    extern __shared__ __align__(16) float rsm[];  // [RMS_NST][RMS_TR][RMS_LD]
-    const int lane = threadIdx.x, tr = lane >> 2, k = lane & 3;
-    const uint32_t row0 = blockIdx.x * RMS_TR;
+    extern __shared__ __align__(16) float rsm_all[];  // [RMS_WARPS][RMS_NST][RMS_TR][RMS_LD]
+    const int lane = threadIdx.x & 31, tr = lane >> 2, k = lane & 3;
+    const uint32_t wg = blockIdx.x * RMS_WARPS + (threadIdx.x >> 5);
+    float* rsm = rsm_all + (size_t)(threadIdx.x >> 5) * RMS_NST * RMS_TR * RMS_LD;
+    const uint32_t row0 = wg * RMS_TR;
+    if (row0 >= nrows) return;  // whole warp idle (warp-level code only below)
     const uint32_t row = row0 + tr;
     const bool live = row < nrows;
     const uint64_t n = live ? row_len[row] : 0;
@@ -560,14 +567,14 @@ void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, ui
 void launch_rms(const void* x, int kind, const uint32_t* row_len, uint32_t nrows, uint64_t pitch,
                 float* frms, uint8_t* status, cudaStream_t st) {
     if (!nrows) return;
-    const size_t smem = (size_t)RMS_NST * RMS_TR * RMS_LD * sizeof(float);
-    const unsigned blocks = (nrows + RMS_TR - 1) / RMS_TR;
+    const size_t smem = (size_t)RMS_WARPS * RMS_NST * RMS_TR * RMS_LD * sizeof(float);
+    const unsigned blocks = (nrows + RMS_TR * RMS_WARPS - 1) / (RMS_TR * RMS_WARPS);
     if (kind == 1) {
         PGB_CUDA(cudaFuncSetAttribute(rms_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rms_kernel<1><<<blocks, 32, smem, st>>>(x, row_len, nrows, pitch, frms, status);
+        rms_kernel<1><<<blocks, 32 * RMS_WARPS, smem, st>>>(x, row_len, nrows, pitch, frms, status);
     } else {
         PGB_CUDA(cudaFuncSetAttribute(rms_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rms_kernel<0><<<blocks, 32, smem, st>>>(x, row_len, nrows, pitch, frms, status);
+        rms_kernel<0><<<blocks, 32 * RMS_WARPS, smem, st>>>(x, row_len, nrows, pitch, frms, status);
     }
     PGB_CUDA(cudaGetLastError());
 }
