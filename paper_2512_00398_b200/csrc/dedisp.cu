@@ -300,7 +300,10 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
 
 constexpr int RING_NS = 3;
 
-template <int G, int VPT>
+// MODE bits (ablation): 1 = byte shifts of the staged copies on the FMA pipe
+// (mul.hi + mad.lo funnel) instead of PRMT on the ALU pipe; 2 = per-(channel, trial)
+// shared-memory addresses formed with IMAD (FMA pipe) instead of IADD (ALU pipe)
+template <int G, int VPT, int MODE>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_u8_ring_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
                           int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
@@ -334,6 +337,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     const uint8_t* rows_i0 = rows + i0;
     constexpr bool kOffs = true;
     const bool offs_thread = (int)threadIdx.x < G * TB / 4;
+    const uint32_t kshift[3] = {p.mul24, p.mul24 >> 8, p.mul24 >> 16};  // 2^24, 2^16, 2^8 (run time)
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
@@ -371,12 +375,25 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
                 *reinterpret_cast<uint4*>(dst) = v0[k];
 #pragma unroll
                 for (int s = 1; s < 4; ++s) {
-                    const uint32_t sel = (uint32_t)(s | (s + 1) << 4 | (s + 2) << 8 | (s + 3) << 12);
                     uint4 sh;
-                    sh.x = __byte_perm(w[0], w[1], sel);
-                    sh.y = __byte_perm(w[1], w[2], sel);
-                    sh.z = __byte_perm(w[2], w[3], sel);
-                    sh.w = __byte_perm(w[3], w[4], sel);
+                    if (MODE & 1) {  // (lo >> 8s) + hi * 2^(32-8s), both on the FMA pipe
+                        const uint32_t km = kshift[s - 1];
+                        uint32_t q[4];
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint32_t t;
+                            asm("mul.hi.u32 %0, %1, %2;" : "=r"(t) : "r"(w[j]), "r"(km));
+                            asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(t) : "r"(w[j + 1]), "r"(km));
+                            q[j] = t;
+                        }
+                        sh = make_uint4(q[0], q[1], q[2], q[3]);
+                    } else {
+                        const uint32_t sel = (uint32_t)(s | (s + 1) << 4 | (s + 2) << 8 | (s + 3) << 12);
+                        sh.x = __byte_perm(w[0], w[1], sel);
+                        sh.y = __byte_perm(w[1], w[2], sel);
+                        sh.z = __byte_perm(w[2], w[3], sel);
+                        sh.w = __byte_perm(w[3], w[4], sel);
+                    }
                     *reinterpret_cast<uint4*>(dst + (size_t)s * W) = sh;
                 }
             }
@@ -450,11 +467,16 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
         ring_wait(full + slot, ph);
         const uint32_t* offb = offs + slot * G * TB + warp * TPW;
         const uint8_t* bufb = buf + (size_t)slot * G * 4 * W + 4 * lane;
+        const uint32_t bufo = (uint32_t)slot * G * 4 * W + 4 * lane;  // byte offset of bufb in smem
 #pragma unroll
         for (int cs = 0; cs < G; ++cs) {
 #pragma unroll
             for (int u = 0; u < TPW; ++u) {
-                const uint8_t* src = bufb + (size_t)cs * 4 * W + offb[cs * TB + u];
+                const uint8_t* src;
+                if (MODE & 2)  // off * 1 + base: one IMAD (FMA pipe) instead of an IADD (ALU)
+                    src = smem + (offb[cs * TB + u] * one + (bufo + (uint32_t)cs * 4 * W));
+                else
+                    src = bufb + (size_t)cs * 4 * W + offb[cs * TB + u];
 #pragma unroll
                 for (int m = 0; m < DD_WORDS; ++m) {
                     const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 128 * m);
@@ -918,6 +940,10 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const char* e = getenv("PGB_DD_RING");
         return !(e && *e == '0');
     }();
+    static const int rmode = [] {  // PGB_RING_MODE: ring-kernel ablation bits (see the kernel)
+        const char* e = getenv("PGB_RING_MODE");
+        return e ? atoi(e) & 3 : 0;
+    }();
     if (ring && !v1 && !sf && p.tpw == 2 && p.dd_off) {
         int g = 8;
         while (g > 1 && ring_smem_bytes(g, p.wmax) > 227 * 1024) g >>= 1;
@@ -925,19 +951,22 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const uint32_t vstride = 32u * (DD_WARPS / g);
         const int vpt = (int)((p.wmax / 16 + vstride - 1) / vstride);
         if (rsm <= 227 * 1024) {
-#define PGB_RING(G_, V_)                                                                          \
-    if (g == G_ && vpt <= V_) {                                                                   \
-        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_kernel<G_, V_>,                              \
+#define PGB_RING3(G_, V_, M_)                                                                     \
+    if (g == G_ && vpt <= V_ && rmode == M_) {                                                    \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_kernel<G_, V_, M_>,                          \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \
-        dedisp_u8_ring_kernel<G_, V_><<<grid, DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len);    \
+        dedisp_u8_ring_kernel<G_, V_, M_><<<grid, DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len);\
         PGB_CUDA(cudaGetLastError());                                                             \
         return;                                                                                   \
     }
+#define PGB_RING(G_, V_) PGB_RING3(G_, V_, 0)
+            PGB_RING3(8, 2, 1) PGB_RING3(8, 2, 2) PGB_RING3(8, 2, 3)
             PGB_RING(8, 1) PGB_RING(8, 2) PGB_RING(8, 4)
             PGB_RING(4, 1) PGB_RING(4, 2) PGB_RING(4, 4)
             PGB_RING(2, 1) PGB_RING(2, 2) PGB_RING(2, 4)
             PGB_RING(1, 1) PGB_RING(1, 2) PGB_RING(1, 4)
 #undef PGB_RING
+#undef PGB_RING3
         }
     }
     if (!v1 && p.tpw == 2 && p.dd_off) {
