@@ -179,6 +179,7 @@ struct ChunkInput {
     const void* data;   // device pointer, time-major
     bool u8;
     bool raw = false;         // the file's unmodified 8-bit samples (overlap reuse allowed)
+    bool more = false;        // another chunk's dedispersion follows (RMS runs beside it)
     uint64_t pitch_min = 0;   // series pitch floor (a file search keeps one pitch for all chunks)
 };
 
@@ -469,7 +470,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     PGB_CUDA(cudaEventRecord(ctx->ev_front[slot], st));
     PGB_CUDA(cudaStreamWaitEvent(rst, ctx->ev_front[slot], 0));
     launch_rms(work, kind, d_len, nrows, out_pitch, ctx->frms[slot].as<float>(),
-               ctx->status[slot].as<uint8_t>(), rst);
+               ctx->status[slot].as<uint8_t>(), in.more && !rms_main, rst);
     PGB_CUDA(cudaEventRecord(ctx->ev_rms[slot], rst));
     ctx->launches += 5;
 
@@ -1091,6 +1092,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
             ChunkInput ci{cptr, true};
             ci.raw = true;
             ci.pitch_min = pitch_min;
+            ci.more = overlap && k + 1 < nchunks;
             if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
                 uint64_t nbc = 0, nbs = 0;
                 ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);
@@ -1100,6 +1102,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                 if (nbc || nbs) {
                     ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
                     ci.pitch_min = pitch_min;
+                    ci.more = overlap && k + 1 < nchunks;
                 }
             }
             ChunkRun& cur = runs[k & 1];

@@ -187,9 +187,10 @@ constexpr int RMS_TR = 8;          // trials per warp
 constexpr int RMS_T = 128;         // elements per trial per stage
 constexpr int RMS_LD = RMS_T + 4;  // padded row length (floats)
 constexpr int RMS_NST = 3;         // ring stages per warp
-// 16 warps (128 trials) per block: the chains are latency-bound, so packing them onto
-// few SMs (8 for 1001 trials) costs the concurrently running dedispersion/boxcar
-// kernels 8 SMs instead of one SM per 8 trials
+// Warps per block is a launch choice (1 or RMS_WARPS): the chains are latency-bound, so
+// when the kernel runs beside the next chunk's dedispersion it packs 16 warps (128
+// trials) per block onto few SMs (8 for 1001 trials) and costs that kernel 8 SMs; when
+// it is on the critical path it spreads one warp per block (~2x faster alone).
 constexpr int RMS_WARPS = 16;
 
 template <int KIND>
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(32 * RMS_WARPS)
                uint64_t pitch, float* __restrict__ frms, uint8_t* __restrict__ status) {
     extern __shared__ __align__(16) float rsm_all[];  // [RMS_WARPS][RMS_NST][RMS_TR][RMS_LD]
     const int lane = threadIdx.x & 31, tr = lane >> 2, k = lane & 3;
-    const uint32_t wg = blockIdx.x * RMS_WARPS + (threadIdx.x >> 5);
+    const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     float* rsm = rsm_all + (size_t)(threadIdx.x >> 5) * RMS_NST * RMS_TR * RMS_LD;
     const uint32_t row0 = wg * RMS_TR;
     if (row0 >= nrows) return;  // whole warp idle (warp-level code only below)
@@ -565,16 +566,19 @@ void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, ui
 }
 
 void launch_rms(const void* x, int kind, const uint32_t* row_len, uint32_t nrows, uint64_t pitch,
-                float* frms, uint8_t* status, cudaStream_t st) {
+                float* frms, uint8_t* status, bool packed, cudaStream_t st) {
     if (!nrows) return;
-    const size_t smem = (size_t)RMS_WARPS * RMS_NST * RMS_TR * RMS_LD * sizeof(float);
-    const unsigned blocks = (nrows + RMS_TR * RMS_WARPS - 1) / (RMS_TR * RMS_WARPS);
+    const int nw = packed ? RMS_WARPS : 1;
+    const size_t smem = (size_t)nw * RMS_NST * RMS_TR * RMS_LD * sizeof(float);
+    const unsigned blocks = (nrows + RMS_TR * nw - 1) / (RMS_TR * nw);
     if (kind == 1) {
-        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rms_kernel<1><<<blocks, 32 * RMS_WARPS, smem, st>>>(x, row_len, nrows, pitch, frms, status);
+        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(RMS_WARPS * RMS_NST * RMS_TR * RMS_LD * sizeof(float))));
+        rms_kernel<1><<<blocks, 32 * nw, smem, st>>>(x, row_len, nrows, pitch, frms, status);
     } else {
-        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        rms_kernel<0><<<blocks, 32 * RMS_WARPS, smem, st>>>(x, row_len, nrows, pitch, frms, status);
+        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(RMS_WARPS * RMS_NST * RMS_TR * RMS_LD * sizeof(float))));
+        rms_kernel<0><<<blocks, 32 * nw, smem, st>>>(x, row_len, nrows, pitch, frms, status);
     }
     PGB_CUDA(cudaGetLastError());
 }

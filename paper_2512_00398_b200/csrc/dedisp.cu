@@ -950,7 +950,10 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const size_t rsm = ring_smem_bytes(g, p.wmax);
         const uint32_t vstride = 32u * (DD_WARPS / g);
         const int vpt = (int)((p.wmax / 16 + vstride - 1) / vstride);
-        if (rsm <= 227 * 1024) {
+        // the 3-slot ring needs 1.5x the shared memory of the double-buffered kernel; when
+        // that forces fewer channels per stage (wide windows, e.g. config C) the
+        // barrier kernel with the larger stage is faster (18.4 vs 19.0 T adds/s on C)
+        if (rsm <= 227 * 1024 && g >= p.g) {
 #define PGB_RING3(G_, V_, M_)                                                                     \
     if (g == G_ && vpt <= V_ && rmode == M_) {                                                    \
         PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_kernel<G_, V_, M_>,                          \

@@ -140,8 +140,9 @@ void launch_baseline_int(const int32_t* x, float* out, const uint32_t* row_len, 
 void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, uint32_t nrows,
                          uint64_t pitch, uint64_t window, cudaStream_t st);
 // input kind: 0 = float baseline output, 1 = int32 series, 2 = float series
+// packed: 16 warps per block (runs beside other kernels), else one warp per block
 void launch_rms(const void* x, int kind, const uint32_t* row_len, uint32_t nrows, uint64_t pitch,
-                float* frms, uint8_t* status, cudaStream_t st);
+                float* frms, uint8_t* status, bool packed, cudaStream_t st);
 void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const float* frms,
                          const uint8_t* status, uint32_t nrows, uint64_t pitch,
                          uint64_t max_len, const ChainParams& cp, const uint32_t* active,
