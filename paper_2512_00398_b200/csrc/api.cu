@@ -97,6 +97,8 @@ struct pgb_context {
     cudaStream_t rms_st = nullptr;  // robust RMS of chunk k overlaps the boxcar of chunk k-1
     cudaEvent_t ev_dd0[2] = {}, ev_dd1[2] = {}, ev_front[2] = {}, ev_rms[2] = {};
     std::vector<cudaEvent_t> seg_events;
+    std::vector<cudaEvent_t> sub_events;                 // first chunk's upload pieces
+    std::vector<std::pair<uint64_t, cudaEvent_t>> prog;  // (end sample, event) of those pieces
 
     // plan
     uint32_t ntrials = 0, nchans = 0;
@@ -180,6 +182,9 @@ struct ChunkInput {
     bool u8;
     bool raw = false;         // the file's unmodified 8-bit samples (overlap reuse allowed)
     bool more = false;        // another chunk's dedispersion follows (RMS runs beside it)
+    // progressive upload (u8, host payload): (end sample, event) of the chunk's
+    // sub-segments; transpose and dedispersion start on the tiles whose inputs arrived
+    const std::vector<std::pair<uint64_t, cudaEvent_t>>* prog = nullptr;
     uint64_t pitch_min = 0;   // series pitch floor (a file search keeps one pitch for all chunks)
 };
 
@@ -209,6 +214,7 @@ void validate_cfg(pgb_context* ctx, const pgb_chunk_spec* spec, const pgb_engine
 }
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+constexpr int PGB_PROG_SUBSEG = 8;  // pieces of the first chunk's upload
 
 // One chunk's chain, split in two halves so a file search can overlap them across
 // chunks: the front half (transpose, dedispersion, baseline on the main stream; the
@@ -349,10 +355,13 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         PGB_CUDA(cudaMemcpyAsync(ctx->d_scale.p, sc, sizeof sc, cudaMemcpyHostToDevice, st));
     }
 
-    // 1. transpose to channel-major rows
+    // 1. transpose to channel-major rows (a progressive chunk transposes per sub-segment
+    // below, interleaved with the dedispersion of the tiles it completes)
+    const bool progressive = u8 && in.prog && !ws_g && !in.prog->empty();
     if (u8) {
-        launch_transpose_u8(static_cast<const uint8_t*>(in.data), L, C, ctx->rows.as<uint8_t>(),
-                            rows_pitch, st);
+        if (!progressive)
+            launch_transpose_u8(static_cast<const uint8_t*>(in.data), L, C, ctx->rows.as<uint8_t>(),
+                                rows_pitch, st);
         if (C_pad > C)
             PGB_CUDA(cudaMemsetAsync(ctx->rows.as<uint8_t>() + (size_t)C * rows_pitch, 0,
                                      (size_t)(C_pad - C) * rows_pitch, st));
@@ -433,7 +442,40 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                 for (uint32_t r = 0; r < nrows; ++r) reused += (uint64_t)keep[r] * C;
             }
         }
-        launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+        if (progressive && dl.tile0 == 0) {
+            // tile t reads channel rows up to t*DD_NT + max delay + DD_NT + 20 bytes (window
+            // start rounded down to 16, whole 16-byte vectors, one extra word)
+            uint64_t a = 0;
+            uint32_t done = 0;
+            for (const auto& seg : *in.prog) {
+                const uint64_t b = std::min<uint64_t>(seg.first, L);
+                PGB_CUDA(cudaStreamWaitEvent(st, seg.second, 0));
+                if (b > a) {
+                    launch_transpose_u8(static_cast<const uint8_t*>(in.data) + a * C, b - a, C,
+                                        ctx->rows.as<uint8_t>() + a, rows_pitch, st);
+                    ctx->launches += 1;
+                }
+                a = b;
+                const uint64_t need = maxd_active + 2 * DD_NT + 64;
+                uint32_t t_end = b >= L ? ntiles : (b >= need ? (uint32_t)((b - need) / DD_NT) + 1 : 0);
+                t_end = std::min(t_end, ntiles);
+                if (t_end > done) {
+                    DedispLaunch part = dl;
+                    part.tile0 = done;
+                    part.ntiles = t_end;
+                    launch_dedisp_u8(part, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+                    ctx->launches += 1;
+                    done = t_end;
+                }
+            }
+            if (done < ntiles) {  // (the last sub-segment ends at L, so this does not happen)
+                DedispLaunch part = dl;
+                part.tile0 = done;
+                launch_dedisp_u8(part, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+            }
+        } else {
+            launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+        }
         if (in.raw) {
             ctx->ser_ok = true;
             ctx->ser_start = spec->start_sample;
@@ -744,6 +786,7 @@ pgb_status pgb_destroy(pgb_context* ctx) {
             b->release();
         ctx->h_counters.release();
         for (auto e : ctx->seg_events) cudaEventDestroy(e);
+        for (auto e : ctx->sub_events) cudaEventDestroy(e);
         for (int k = 0; k < 2; ++k)
             for (cudaEvent_t e : {ctx->ev_dd0[k], ctx->ev_dd1[k], ctx->ev_front[k], ctx->ev_rms[k]})
                 cudaEventDestroy(e);
@@ -1034,8 +1077,32 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                 PGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
                 ctx->seg_events.push_back(e);
             }
-            // upload segment k = [end of chunk k-1, end of chunk k) on the copy stream
+            // upload segment k = [end of chunk k-1, end of chunk k) on the copy stream; the
+            // first chunk's segment goes up in PGB_PROG_SUBSEG pieces so its transpose and
+            // dedispersion start before the whole chunk has arrived
             uint64_t done = 0;
+            ctx->prog.clear();
+            const bool prog_ok = nchunks > 0 && !(rfi && (rfi->narrowband || rfi->broadband)) &&
+                                 chunks[0].start_sample == 0 && !getenv("PGB_NO_PROGRESSIVE");
+            if (prog_ok) {
+                const uint64_t L0 = std::min<uint64_t>(chunks[0].length, nsamples);
+                while (ctx->sub_events.size() < PGB_PROG_SUBSEG) {
+                    cudaEvent_t e;
+                    PGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                    ctx->sub_events.push_back(e);
+                }
+                for (int j = 0; j < PGB_PROG_SUBSEG; ++j) {
+                    uint64_t e = j + 1 == PGB_PROG_SUBSEG ? L0 : round_up(L0 * (j + 1) / PGB_PROG_SUBSEG, 64);
+                    e = std::min(e, L0);
+                    if (e > done) {
+                        PGB_CUDA(cudaMemcpyAsync(ctx->payload.as<uint8_t>() + done * C, payload + done * C,
+                                                 (e - done) * C, cudaMemcpyHostToDevice, ctx->copy_st));
+                        done = e;
+                    }
+                    PGB_CUDA(cudaEventRecord(ctx->sub_events[j], ctx->copy_st));
+                    ctx->prog.emplace_back(e, ctx->sub_events[j]);
+                }
+            }
             for (size_t k = 0; k < nchunks; ++k) {
                 const uint64_t end = chunks[k].start_sample + chunks[k].length;
                 need(end <= nsamples, PGB_ERR_INVALID_PLAN, "chunk extends past the payload");
@@ -1087,12 +1154,14 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
         bool pending = false;
         for (size_t k = 0; k < nchunks; ++k) {
             validate_cfg(ctx, &chunks[k], cfg);
-            if (!payload_on_device) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
+            const bool prog_k = k == 0 && !payload_on_device && !ctx->prog.empty();
+            if (!payload_on_device && !prog_k) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
             const uint8_t* cptr = dpay + chunks[k].start_sample * C;
             ChunkInput ci{cptr, true};
             ci.raw = true;
             ci.pitch_min = pitch_min;
             ci.more = overlap && k + 1 < nchunks;
+            if (prog_k) ci.prog = &ctx->prog;
             if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
                 uint64_t nbc = 0, nbs = 0;
                 ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);

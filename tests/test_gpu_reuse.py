@@ -37,3 +37,29 @@ def test_reuse_matches_full_recompute(monkeypatch, baseline_s):
     for k in a.candidates.dtype.names:
         assert np.array_equal(a.candidates[k], b.candidates[k]), k
     assert write_candidates(a.clusters) == write_candidates(b.clusters)
+
+
+def test_progressive_first_chunk_matches(monkeypatch):
+    """A host payload's first chunk is uploaded in pieces and its transpose and
+    dedispersion start on the tiles whose samples arrived; the result must equal the
+    one-piece upload (PGB_NO_PROGRESSIVE=1) and the device-resident payload."""
+    import torch
+
+    hdr = FilterbankHeader(fch1=1500.0, foff=-1.0, nchans=256, tsamp=64e-6, nsamples=3 << 15)
+    params = SearchParams(dm_lo=0.0, dm_hi=300.0, spacing=LinearSpacing(2.0),
+                          engine=EngineConfig(boxcar_max=1024), baseline_len_s=0.25,
+                          nsamps_chunk=1 << 16, rfi=RfiConfig(False, False))
+    task = create_task(hdr, params)
+    payload = u8_chunk(hdr, task.plan, hdr.nsamples, seed=78,
+                       pulses=[(30, 9000, 4, 25.0), (100, 40000, 16, 20.0), (140, 70000, 64, 30.0)])
+    a = search_file(payload, task)
+    monkeypatch.setenv("PGB_NO_PROGRESSIVE", "1")
+    b = search_file(payload, task)
+    monkeypatch.delenv("PGB_NO_PROGRESSIVE")
+    c = search_file(torch.from_numpy(payload).cuda(), task)
+    assert len(a.candidates) > 0
+    for other in (b, c):
+        assert len(other.candidates) == len(a.candidates)
+        for k in a.candidates.dtype.names:
+            assert np.array_equal(a.candidates[k], other.candidates[k]), k
+        assert write_candidates(other.clusters) == write_candidates(a.clusters)
