@@ -16,6 +16,8 @@
 //   5. clusters sorted by the representative's packed (peak, trial, width) key.
 #include <cub/device/device_radix_sort.cuh>
 
+#include <cstdlib>
+
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -161,6 +163,71 @@ __global__ void link_kernel(const pgb_candidate* __restrict__ c, uint64_t n, Cel
             }
         }
     }
+}
+
+// Small sets (n <= LINK_SMEM_MAX): the same linking with the union-find forest in
+// shared memory, one CTA.  The global version's finds are chains of uncached L2 loads
+// (~0.5 us each), which made a config-B link_grid (~600 candidates in a few dense
+// cells) take ~1.9 ms; here a find is a few shared-memory loads.  The hooking rule
+// (parent[max] = min) and therefore the forest's roots are the same.
+constexpr uint32_t LINK_SMEM_MAX = 12288;
+
+__device__ uint32_t suf_find(uint32_t* parent, uint32_t x) {
+    for (;;) {
+        const uint32_t p = ((volatile uint32_t*)parent)[x];
+        if (p == x) return x;
+        const uint32_t gp = ((volatile uint32_t*)parent)[p];
+        if (gp != p) ((volatile uint32_t*)parent)[x] = gp;
+        x = gp;
+    }
+}
+
+__device__ void suf_unite(uint32_t* parent, uint32_t a, uint32_t b) {
+    for (;;) {
+        a = suf_find(parent, a);
+        b = suf_find(parent, b);
+        if (a == b) return;
+        if (a > b) {
+            const uint32_t t = a;
+            a = b;
+            b = t;
+        }
+        const uint32_t old = atomicCAS(&parent[b], b, a);
+        if (old == b) return;
+        b = old;
+    }
+}
+
+__global__ void __launch_bounds__(1024)
+    link_smem_kernel(const pgb_candidate* __restrict__ c, uint32_t n, CellGeom g,
+                     const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx,
+                     uint32_t* parent_out) {
+    __shared__ uint32_t parent[LINK_SMEM_MAX];
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) parent[i] = i;
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const pgb_candidate a = c[i];
+        const int64_t kt = (int64_t)(a.peak_sample / g.cell_t());
+        const int64_t kd = (int64_t)(a.dm_trial / g.cell_dm());
+        const int64_t kw = (int64_t)(a.width_index / g.cell_w());
+        for (int64_t dt = -1; dt <= 1; ++dt) {
+            if (kt + dt < 0) continue;
+            for (int64_t dd = -1; dd <= 1; ++dd) {
+                if (kd + dd < 0) continue;
+                for (int64_t dw = -1; dw <= 1; ++dw) {
+                    if (kw + dw < 0) continue;
+                    const uint64_t key = cell_key(kt + dt, kd + dd, kw + dw);
+                    uint64_t p = lower_bound(skeys, n, key);
+                    for (; p < n && skeys[p] == key; ++p) {
+                        const uint32_t j = sidx[p];
+                        if (j > i && linked(a, c[j], g.r)) suf_unite(parent, i, j);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) parent_out[i] = suf_find(parent, i);
 }
 
 __global__ void rank_kernel(const uint32_t* __restrict__ sorted_idx, uint64_t n, uint32_t* rank) {
@@ -313,7 +380,10 @@ void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_r
     cub::DoubleBuffer<uint64_t> ck(keys_a, keys_b);
     cub::DoubleBuffer<uint32_t> cv(idx_a, idx_b);
     PGB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, sort_tmp, ck, cv, (int)n, 0, 64, st));
-    link_kernel<<<nblk(n), 256, 0, st>>>(cands, n, g, ck.Current(), cv.Current(), parent);
+    if (n <= LINK_SMEM_MAX && !getenv("PGB_LINK_GLOBAL"))
+        link_smem_kernel<<<1, 1024, 0, st>>>(cands, (uint32_t)n, g, ck.Current(), cv.Current(), parent);
+    else
+        link_kernel<<<nblk(n), 256, 0, st>>>(cands, n, g, ck.Current(), cv.Current(), parent);
     // 3. ranks by (peak, trial, input index); representative and extents
     cub::DoubleBuffer<uint64_t> rk(rkeys_a, rkeys_b);
     cub::DoubleBuffer<uint32_t> rv(ridx_a, ridx_b);

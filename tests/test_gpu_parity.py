@@ -244,6 +244,21 @@ def test_link_grid_vs_reference_library(engine, ref):
     clusters_equal(got, recs, members)
 
 
+@pytest.mark.parametrize("n,extent", [(3000, 20_000), (12288, 2_000_000), (20000, 3_000_000)])
+def test_link_grid_smem_and_global_forests_agree(engine, port, monkeypatch, n, extent):
+    """link_grid links sets of <= 12288 candidates with a shared-memory union-find and
+    larger ones with the global one; both must give the reference clusters (dense sets
+    make big components and contended unions)."""
+    rng = np.random.default_rng(n)
+    cands = random_candidates(rng, n, extent)
+    a = engine.link_grid(cands, LinkRadii())
+    monkeypatch.setenv("PGB_LINK_GLOBAL", "1")
+    b = engine.link_grid(cands, LinkRadii())
+    recs, members = port.link_grid(cands, (3, 9, 3))
+    clusters_equal(a, recs, members)
+    clusters_equal(b, recs, members)
+
+
 def test_link_grid_ties(engine):
     # tests/test_cluster.cpp:92-100
     from paper_2512_00398_b200 import abi
