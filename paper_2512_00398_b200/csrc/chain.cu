@@ -19,6 +19,8 @@
 //     that a second kernel stitches after a device sort.
 #include <cuda_pipeline.h>
 
+#include <algorithm>
+
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -184,23 +186,30 @@ __device__ __forceinline__ float load_x(const void* base, size_t idx) {
 // reads 16 values ahead of its add chain.  Both passes (sum of squares, then the
 // 3-sigma-clipped sum) run in the same kernel.
 constexpr int RMS_TR = 8;          // trials per warp
-constexpr int RMS_T = 128;         // elements per trial per stage
-constexpr int RMS_LD = RMS_T + 4;  // padded row length (floats)
-constexpr int RMS_NST = 3;         // ring stages per warp
-// Warps per block is a launch choice (1 or RMS_WARPS): the chains are latency-bound, so
-// when the kernel runs beside the next chunk's dedispersion it packs 16 warps (128
-// trials) per block onto few SMs (8 for 1001 trials) and costs that kernel 8 SMs; when
-// it is on the critical path it spreads one warp per block (~2x faster alone).
+// Warps per block is a launch choice: the chains are latency-bound, so when the kernel
+// runs beside the next chunk's dedispersion it packs up to 16 warps per block (~8
+// blocks) onto few SMs with short stages (RT = 128 samples per trial); when it is on
+// the critical path it spreads one warp per block with long stages (RT = 512).
 constexpr int RMS_WARPS = 16;
+#ifndef RMS_U
+#define RMS_U 16  // values loaded and converted ahead of the add chain
+#endif
 
-template <int KIND>
+template <int RT, int NST>
+constexpr size_t rms_warp_smem() { return (size_t)NST * RMS_TR * (RT + 4) * sizeof(float); }
+
+// NST: cp.async ring stages per warp (a lone warp on an SM needs a deep ring to keep
+// enough bytes in flight for its 8 trials)
+template <int KIND, int RT, int NST>
 __global__ void __launch_bounds__(32 * RMS_WARPS)
     rms_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len, uint32_t nrows,
                uint64_t pitch, float* __restrict__ frms, uint8_t* __restrict__ status) {
-    extern __shared__ __align__(16) float rsm_all[];  // [RMS_WARPS][RMS_NST][RMS_TR][RMS_LD]
+    constexpr int LD = RT + 4;      // padded row length (floats): the 32 lanes hit 32 banks
+    constexpr int Q = RT / 128;     // float4 copies per lane per row and stage
+    extern __shared__ __align__(16) float rsm_all[];  // [warps][NST][RMS_TR][LD]
     const int lane = threadIdx.x & 31, tr = lane >> 2, k = lane & 3;
     const uint32_t wg = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-    float* rsm = rsm_all + (size_t)(threadIdx.x >> 5) * RMS_NST * RMS_TR * RMS_LD;
+    float* rsm = rsm_all + (size_t)(threadIdx.x >> 5) * NST * RMS_TR * LD;
     const uint32_t row0 = wg * RMS_TR;
     if (row0 >= nrows) return;  // whole warp idle (warp-level code only below)
     const uint32_t row = row0 + tr;
@@ -209,18 +218,21 @@ __global__ void __launch_bounds__(32 * RMS_WARPS)
     const uint64_t nq4 = n & ~3ull;  // elements covered by the 4-chain loop
     uint64_t nmax = n;
     for (int o = 16; o; o >>= 1) nmax = max(nmax, (uint64_t)__shfl_xor_sync(0xffffffffu, nmax, o));
-    const uint64_t nstages = (nmax + RMS_T - 1) / RMS_T;
-    const char* base = static_cast<const char*>(x_all);
+    const uint64_t nstages = (nmax + RT - 1) / RT;
+    // source rows of this warp's 8 trials (rows past nrows repeat the last one)
+    const float* rowp[RMS_TR];
+#pragma unroll
+    for (int r = 0; r < RMS_TR; ++r)
+        rowp[r] = static_cast<const float*>(x_all) + (size_t)min(row0 + r, nrows - 1) * pitch + 4 * lane;
 
     auto issue = [&](uint64_t st) {
         if (st < nstages) {
-            float* dst = rsm + (st % RMS_NST) * RMS_TR * RMS_LD;
-            for (int v = lane; v < RMS_TR * (RMS_T / 4); v += 32) {
-                const int r = v / (RMS_T / 4), e4 = v % (RMS_T / 4);
-                const uint32_t rr = min(row0 + r, nrows - 1);
-                const char* src = base + ((size_t)rr * pitch + st * RMS_T + 4 * e4) * 4;
-                __pipeline_memcpy_async(dst + r * RMS_LD + 4 * e4, src, 16);
-            }
+            float* dst = rsm + (st % NST) * RMS_TR * LD + 4 * lane;
+#pragma unroll
+            for (int r = 0; r < RMS_TR; ++r)
+#pragma unroll
+                for (int q = 0; q < Q; ++q)
+                    __pipeline_memcpy_async(dst + r * LD + 128 * q, rowp[r] + st * RT + 128 * q, 16);
         }
         __pipeline_commit();
     };
@@ -230,32 +242,36 @@ __global__ void __launch_bounds__(32 * RMS_WARPS)
     float cut = 0.0f;
     double rms0 = 0.0;
     for (int pass = 0; pass < 2; ++pass) {
-        for (int st = 0; st < RMS_NST - 1; ++st) issue(st);
+        for (int st = 0; st < NST - 1; ++st) issue(st);
         for (uint64_t st = 0; st < nstages; ++st) {
-            issue(st + RMS_NST - 1);
-            __pipeline_wait_prior(RMS_NST - 1);
+            issue(st + NST - 1);
+            __pipeline_wait_prior(NST - 1);
             __syncwarp();
-            const float* t = rsm + (st % RMS_NST) * RMS_TR * RMS_LD + tr * RMS_LD;
-            const uint64_t i0 = st * RMS_T;
-            const int jmax = nq4 > i0 ? (int)min((uint64_t)RMS_T, nq4 - i0) : 0;
+            const float* t = rsm + (st % NST) * RMS_TR * LD + tr * LD;
+            const uint64_t i0 = st * RT;
+            const int jmax = nq4 > i0 ? (int)min((uint64_t)RT, nq4 - i0) : 0;
             int j = k;
-            for (; j + 60 < jmax; j += 64) {  // 16 values ahead of the add chain
-                float v[16];
+            for (; j + 4 * (RMS_U - 1) < jmax; j += 4 * RMS_U) {  // RMS_U values ahead of the chain
+                float v[RMS_U];
 #pragma unroll
-                for (int u = 0; u < 16; ++u) {
+                for (int u = 0; u < RMS_U; ++u) {
                     const float f = t[j + 4 * u];
                     v[u] = KIND == 1 ? (float)__float_as_int(f) : f;
                 }
                 // double(v)*double(v) is exact (24+24 significant bits), so the
-                // reference's a += v*v (one rounding) is exactly one DFMA
+                // reference's a += v*v (one rounding) is one DFMA, or an exact DMUL off
+                // the chain plus one DADD on it.  Pass 2 adds +0.0 for clipped samples:
+                // b is a sum of squares (never -0), so b + 0.0 == b and the chain is one
+                // DADD per sample instead of DFMA + select.
 #pragma unroll
-                for (int u = 0; u < 16; ++u) {
+                for (int u = 0; u < RMS_U; ++u) {
                     const double dv = (double)v[u];
                     if (pass == 0) {
                         a = __fma_rn(dv, dv, a);
-                    } else if (fabsf(v[u]) <= cut) {
-                        b = __fma_rn(dv, dv, b);
-                        ++kept;
+                    } else {
+                        const bool keep = fabsf(v[u]) <= cut;
+                        b = __dadd_rn(b, keep ? __dmul_rn(dv, dv) : 0.0);
+                        kept += keep;
                     }
                 }
             }
@@ -568,18 +584,27 @@ void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, ui
 void launch_rms(const void* x, int kind, const uint32_t* row_len, uint32_t nrows, uint64_t pitch,
                 float* frms, uint8_t* status, bool packed, cudaStream_t st) {
     if (!nrows) return;
-    const int nw = packed ? RMS_WARPS : 1;
-    const size_t smem = (size_t)nw * RMS_NST * RMS_TR * RMS_LD * sizeof(float);
+    // packed: about 8 blocks (1001 trials: 16 warps each; a 125-trial shard: 2 each), so the
+    // chains stay on few SMs without stacking so many warps per SM that they slow down
+    const uint32_t nwarps = (nrows + RMS_TR - 1) / RMS_TR;
+    const int nw = packed ? (int)std::min<uint32_t>(RMS_WARPS, std::max<uint32_t>(1, nwarps / 8)) : 1;
     const unsigned blocks = (nrows + RMS_TR * nw - 1) / (RMS_TR * nw);
-    if (kind == 1) {
-        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(RMS_WARPS * RMS_NST * RMS_TR * RMS_LD * sizeof(float))));
-        rms_kernel<1><<<blocks, 32 * nw, smem, st>>>(x, row_len, nrows, pitch, frms, status);
+#define PGB_RMS(K, RT, NS)                                                                         \
+    do {                                                                                           \
+        const size_t smem = (size_t)nw * rms_warp_smem<RT, NS>();                                  \
+        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<K, RT, NS>,                                       \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+        rms_kernel<K, RT, NS><<<blocks, 32 * nw, smem, st>>>(x, row_len, nrows, pitch, frms, status); \
+    } while (0)
+    // a warp's ring: 99 KB at RT 512 x 6 stages (one warp per block), 12.4 KB at 128 x 3
+    if (nw == 1) {
+        if (kind == 1) PGB_RMS(1, 512, 6);
+        else PGB_RMS(0, 512, 6);
     } else {
-        PGB_CUDA(cudaFuncSetAttribute(rms_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                      (int)(RMS_WARPS * RMS_NST * RMS_TR * RMS_LD * sizeof(float))));
-        rms_kernel<0><<<blocks, 32 * nw, smem, st>>>(x, row_len, nrows, pitch, frms, status);
+        if (kind == 1) PGB_RMS(1, 128, 3);
+        else PGB_RMS(0, 128, 3);
     }
+#undef PGB_RMS
     PGB_CUDA(cudaGetLastError());
 }
 
