@@ -13,6 +13,8 @@
 #include <numeric>
 #include <stdexcept>
 
+#include <cstdio>
+
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -126,13 +128,28 @@ struct pgb_context {
     uint64_t ser_start = 0, ser_len = 0, ser_pitch = 0;
     uint32_t dd_tab_wmax = 0;  // wmax the staging table was built for (0 = stale)
     DevBuf file_cands, file_sorted;
+    // asynchronous file-search back halves: {candidate total, high-water nc, nf}, the
+    // per-chunk degenerate-trial flags (pinned) and per-chunk dedispersion events
+    DevBuf file_ctr;
+    PinnedBuf h_file_status, h_file_ctr;
+    std::vector<cudaEvent_t> file_dd_ev;
+    // pinned staging arena for the small per-chunk uploads (a pageable cudaMemcpyAsync
+    // waited for the RMS kernel running on the other stream, stalling the next chunk's
+    // dedispersion); bump-allocated, reset at the start of every top-level call
+    std::vector<PinnedBuf> stage;
+    size_t stage_blk = 0, stage_off = 0;
+    // PGB_TRACE=1: an event after each stage of a file search, printed as a timeline
+    bool trace = false;
+    std::vector<std::pair<std::string, cudaEvent_t>> trace_ev;
     DevBuf cl_scratch, clusters, members;
     PinnedBuf h_counters;
     RfiWork rfi;
     DevBuf rfi_out;
     uint64_t rfi_len = 0;
 
-    uint64_t cand_cap = 1 << 16, frag_cap = 1 << 16;
+    // per-chunk candidate / fragment buffers; the file search sorts whole buffers (device-side
+    // counts), so they start moderate and grow on overflow
+    uint64_t cand_cap = 1 << 14, frag_cap = 1 << 14;
 
     // results
     uint64_t n_cands = 0;
@@ -185,6 +202,7 @@ struct ChunkInput {
     // progressive upload (u8, host payload): (end sample, event) of the chunk's
     // sub-segments; transpose and dedispersion start on the tiles whose inputs arrived
     const std::vector<std::pair<uint64_t, cudaEvent_t>>* prog = nullptr;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // dedispersion timing events (else the slot's)
     uint64_t pitch_min = 0;   // series pitch floor (a file search keeps one pitch for all chunks)
 };
 
@@ -214,6 +232,59 @@ void validate_cfg(pgb_context* ctx, const pgb_chunk_spec* spec, const pgb_engine
 }
 
 uint64_t round_up(uint64_t v, uint64_t a) { return (v + a - 1) / a * a; }
+
+void stage_reset(pgb_context* ctx) {
+    ctx->stage_blk = 0;
+    ctx->stage_off = 0;
+}
+
+// H2D copy of a small host array through the pinned arena (asynchronous for real)
+void stage_h2d(pgb_context* ctx, void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (!bytes) return;
+    const size_t need = (bytes + 255) & ~size_t(255);
+    constexpr size_t kBlock = 4u << 20;
+    while (true) {
+        if (ctx->stage_blk == ctx->stage.size()) {
+            ctx->stage.emplace_back();
+            ctx->stage.back().reserve(std::max(kBlock, need));
+            ctx->stage_off = 0;
+        }
+        PinnedBuf& b = ctx->stage[ctx->stage_blk];
+        if (ctx->stage_off + need <= b.bytes) break;
+        ++ctx->stage_blk;
+        ctx->stage_off = 0;
+        if (ctx->stage_blk < ctx->stage.size() && ctx->stage[ctx->stage_blk].bytes < need)
+            ctx->stage[ctx->stage_blk].reserve(need);  // (not in use: blocks past the cursor are free)
+    }
+    char* p = ctx->stage[ctx->stage_blk].as<char>() + ctx->stage_off;
+    ctx->stage_off += need;
+    std::memcpy(p, src, bytes);
+    // the device reads the pinned bytes itself (zero copy): a cudaMemcpyAsync would queue
+    // behind the multi-GB payload segments on the H2D copy engine
+    launch_copy_from_host(dst, p, bytes, st);
+}
+
+void trace_mark(pgb_context* ctx, const char* name, cudaStream_t s) {
+    if (!ctx->trace) return;
+    cudaEvent_t e;
+    PGB_CUDA(cudaEventCreate(&e));
+    PGB_CUDA(cudaEventRecord(e, s));
+    ctx->trace_ev.emplace_back(std::string(name) + (s == ctx->st ? "" : " [side stream]"), e);
+}
+
+void trace_dump(pgb_context* ctx) {
+    if (!ctx->trace || ctx->trace_ev.empty()) return;
+    PGB_CUDA(cudaDeviceSynchronize());
+    float prev = 0.f;
+    for (auto& [name, e] : ctx->trace_ev) {
+        float t = 0.f;
+        PGB_CUDA(cudaEventElapsedTime(&t, ctx->trace_ev.front().second, e));
+        fprintf(stderr, "[pgb trace] %9.3f ms  +%8.3f  %s\n", t, t - prev, name.c_str());
+        prev = t;
+    }
+    for (auto& [name, e] : ctx->trace_ev) cudaEventDestroy(e);
+    ctx->trace_ev.clear();
+}
 constexpr int PGB_PROG_SUBSEG = 8;  // pieces of the first chunk's upload
 
 // One chunk's chain, split in two halves so a file search can overlap them across
@@ -291,8 +362,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         ctx->geom_valid = true;
         ctx->dd_tab_wmax = 0;
         ctx->d_active.reserve(nrows * sizeof(uint32_t));
-        PGB_CUDA(cudaMemcpyAsync(ctx->d_active.p, active.data(), nrows * sizeof(uint32_t),
-                                 cudaMemcpyHostToDevice, st));
+        stage_h2d(ctx, ctx->d_active.p, active.data(), nrows * sizeof(uint32_t), st);
     }
     std::vector<uint32_t> blk_len(nblocks, 0);
     for (uint32_t r = 0; r < nrows; ++r) blk_len[r / tb] = std::max(blk_len[r / tb], row_len[r]);
@@ -341,18 +411,15 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     ctx->d_row_len[slot].reserve(nrows * sizeof(uint32_t));
     ctx->slot_active[slot].reserve(nrows * sizeof(uint32_t));
     ctx->d_blk_len.reserve(nblocks * sizeof(uint32_t));
-    PGB_CUDA(cudaMemcpyAsync(ctx->d_row_len[slot].p, row_len.data(), nrows * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice, st));
-    PGB_CUDA(cudaMemcpyAsync(ctx->slot_active[slot].p, active.data(), nrows * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice, st));
-    PGB_CUDA(cudaMemcpyAsync(ctx->d_blk_len.p, blk_len.data(), nblocks * sizeof(uint32_t),
-                             cudaMemcpyHostToDevice, st));
+    stage_h2d(ctx, ctx->d_row_len[slot].p, row_len.data(), nrows * sizeof(uint32_t), st);
+    stage_h2d(ctx, ctx->slot_active[slot].p, active.data(), nrows * sizeof(uint32_t), st);
+    stage_h2d(ctx, ctx->d_blk_len.p, blk_len.data(), nblocks * sizeof(uint32_t), st);
     // ladder scales 1/sqrt(w) (src/engine.cpp:207), computed on the host like the reference
     {
         double sc[32];
         for (int l = 0; l < 32; ++l) sc[l] = 1.0 / std::sqrt((double)(1ull << l));
         ctx->d_scale.reserve(sizeof sc);
-        PGB_CUDA(cudaMemcpyAsync(ctx->d_scale.p, sc, sizeof sc, cudaMemcpyHostToDevice, st));
+        stage_h2d(ctx, ctx->d_scale.p, sc, sizeof sc, st);
     }
 
     // 1. transpose to channel-major rows (a progressive chunk transposes per sub-segment
@@ -362,6 +429,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         if (!progressive)
             launch_transpose_u8(static_cast<const uint8_t*>(in.data), L, C, ctx->rows.as<uint8_t>(),
                                 rows_pitch, st);
+        trace_mark(ctx, "transpose", st);
         if (C_pad > C)
             PGB_CUDA(cudaMemsetAsync(ctx->rows.as<uint8_t>() + (size_t)C * rows_pitch, 0,
                                      (size_t)(C_pad - C) * rows_pitch, st));
@@ -386,7 +454,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     dl.ntiles = ntiles;
     dl.mul24 = 1u << 24;
     uint64_t reused = 0;  // channel-adds taken over from the previous chunk
-    PGB_CUDA(cudaEventRecord(ctx->ev_dd0[slot], st));
+    PGB_CUDA(cudaEventRecord(in.ev0 ? in.ev0 : ctx->ev_dd0[slot], st));
     if (u8 && ws_g) {
         DedispLaunch dw = dl;
         dw.g = ws_g;
@@ -433,9 +501,10 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                 const uint32_t tile0 = *std::min_element(first.begin(), first.end());
                 ctx->d_keep.reserve((size_t)(nrows + nblocks) * sizeof(uint32_t));
                 uint32_t* dk = ctx->d_keep.as<uint32_t>();
-                PGB_CUDA(cudaMemcpyAsync(dk, keep.data(), nrows * 4, cudaMemcpyHostToDevice, st));
-                PGB_CUDA(cudaMemcpyAsync(dk + nrows, first.data(), nblocks * 4, cudaMemcpyHostToDevice, st));
+                stage_h2d(ctx, dk, keep.data(), nrows * 4, st);
+                stage_h2d(ctx, dk + nrows, first.data(), nblocks * 4, st);
                 launch_series_shift(ctx->series.as<int32_t>(), nrows, out_pitch, shift, dk, st);
+                trace_mark(ctx, "series shift", st);
                 ctx->launches += 1;
                 dl.blk_first = dk + nrows;
                 dl.tile0 = tile0;
@@ -484,7 +553,8 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         }
     }
     else launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
-    PGB_CUDA(cudaEventRecord(ctx->ev_dd1[slot], st));
+    PGB_CUDA(cudaEventRecord(in.ev1 ? in.ev1 : ctx->ev_dd1[slot], st));
+    trace_mark(ctx, "dedispersion", st);
     ctx->dedisp_launches += 1;
     ctx->launches += 2;
     uint64_t adds = 0;
@@ -507,6 +577,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         work = ctx->base[slot].p;
         kind = 0;
     }
+    trace_mark(ctx, "baseline", st);
     static const bool rms_main = getenv("PGB_RMS_MAIN") != nullptr;  // experiment: no overlap
     cudaStream_t rst = rms_main ? st : ctx->rms_st;
     PGB_CUDA(cudaEventRecord(ctx->ev_front[slot], st));
@@ -514,6 +585,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     launch_rms(work, kind, d_len, nrows, out_pitch, ctx->frms[slot].as<float>(),
                ctx->status[slot].as<uint8_t>(), in.more && !rms_main, rst);
     PGB_CUDA(cudaEventRecord(ctx->ev_rms[slot], rst));
+    trace_mark(ctx, "robust rms", rst);
     ctx->launches += 5;
 
     run.live = true;
@@ -628,6 +700,63 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
     ctx->last_u8 = run.u8;
 }
 
+// File-search back half without host round trips (the synchronous chunk_back reads the
+// run/candidate counts back three times per chunk, idling the GPU while the host issues
+// the next launches): fixed capacities and device-side counts for the fragment and
+// candidate sorts, candidates appended to ctx->file_cands at a device-side total, the
+// degenerate-trial flags copied to pinned host memory.  The file search reads all of it
+// once at the end and re-runs the file with larger capacities if a counter overflowed.
+void chunk_back_async(pgb_context* ctx, ChunkRun& run, uint8_t* h_status, uint64_t file_cap) {
+    cudaStream_t st = ctx->st;
+    const int slot = run.slot;
+    if (!run.live) return;
+    const pgb_chunk_spec* spec = &run.spec;
+    const pgb_engine_config* cfg = &run.cfg;
+    PGB_CUDA(cudaStreamWaitEvent(st, ctx->ev_rms[slot], 0));
+    ChainParams cp{};
+    cp.start_sample = spec->start_sample;
+    cp.valid_begin = spec->valid_begin;
+    cp.valid_end = spec->valid_end;
+    cp.drop_left = spec->start_sample > 0;
+    cp.drop_right = spec->overlap > 0;
+    cp.tsamp = cfg->tsamp;
+    cp.threshold = (double)cfg->detect_thresh;
+    cp.boxcar_max = cfg->boxcar_max;
+    const uint64_t ccap = ctx->cand_cap, fcap = ctx->frag_cap, cap = std::max(ccap, fcap);
+    ctx->counters.reserve(4 * sizeof(unsigned long long));
+    auto* dcnt = ctx->counters.as<unsigned long long>();
+    ctx->cands_raw.reserve(ccap * sizeof(pgb_candidate));
+    ctx->cands_sorted.reserve(ccap * sizeof(pgb_candidate));
+    ctx->frags.reserve(fcap * sizeof(Fragment));
+    ctx->frags_sorted.reserve(fcap * sizeof(Fragment));
+    const size_t tmp = sort_fragments_temp_bytes(cap);
+    ctx->sort_tmp.reserve(tmp);
+    ctx->sort_keys.reserve(2 * cap * sizeof(uint64_t));
+    ctx->sort_idx.reserve(2 * cap * sizeof(uint32_t));
+    uint64_t* ka = ctx->sort_keys.as<uint64_t>();
+    uint32_t* ia = ctx->sort_idx.as<uint32_t>();
+    PGB_CUDA(cudaMemsetAsync(dcnt, 0, 2 * sizeof(unsigned long long), st));
+    launch_boxcar_peaks(run.work, run.kind, ctx->d_row_len[slot].as<uint32_t>(), ctx->frms[slot].as<float>(),
+                        ctx->status[slot].as<uint8_t>(), run.nrows, run.out_pitch, run.max_n, cp,
+                        ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
+                        ctx->d_scale.as<double>(), ctx->cands_raw.as<pgb_candidate>(), dcnt, ccap,
+                        ctx->frags.as<Fragment>(), dcnt + 1, fcap, st);
+    trace_mark(ctx, "boxcar + runs", st);
+    sort_fragments_dev(ctx->frags.as<Fragment>(), ctx->frags_sorted.as<Fragment>(), fcap, dcnt + 1,
+                       ctx->sort_tmp.p, tmp, ka, ka + cap, ia, ia + cap, st);
+    launch_stitch_dev(ctx->frags_sorted.as<Fragment>(), fcap, dcnt + 1, ctx->d_row_len[slot].as<uint32_t>(),
+                      cp, ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
+                      ctx->cands_raw.as<pgb_candidate>(), dcnt, ccap, st);
+    sort_candidates_dev(ctx->cands_raw.as<pgb_candidate>(), ctx->cands_sorted.as<pgb_candidate>(), ccap,
+                        dcnt, ctx->sort_tmp.p, tmp, ka, ka + cap, ia, ia + cap, st);
+    auto* fc = ctx->file_ctr.as<unsigned long long>();
+    append_candidates_dev(ctx->cands_sorted.as<pgb_candidate>(), ccap, dcnt,
+                          ctx->file_cands.as<pgb_candidate>(), fc, file_cap, fc + 1, st);
+    PGB_CUDA(cudaMemcpyAsync(h_status, ctx->status[slot].p, run.nrows, cudaMemcpyDeviceToHost, st));
+    trace_mark(ctx, "fragment/candidate order + append", st);
+    ctx->launches += 12;
+}
+
 // Runs the whole chain for one chunk whose samples are already on the device.
 void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spec,
                const pgb_engine_config* cfg) {
@@ -662,6 +791,10 @@ RfiParams to_rfi(const pgb_rfi_config* r) {
 }
 
 void reset_timing(pgb_context* ctx) {
+    // every top-level call starts here (after the previous call's final stream sync), so
+    // the staging arena is free again
+    ctx->stage_blk = 0;
+    ctx->stage_off = 0;
     ctx->dedisp_ms = 0.0;
     ctx->dedisp_launches = 0;
     ctx->channel_adds = 0;
@@ -752,6 +885,10 @@ pgb_status pgb_create(int device, pgb_context** out) {
                                          prop.name);
         auto* ctx = new pgb_context();
         ctx->device = device;
+        if (const char* e = getenv("PGB_INITIAL_CAP")) {  // tests: start the candidate/fragment
+            const uint64_t c = strtoull(e, nullptr, 10);   // buffers small to force the growth paths
+            if (c) ctx->cand_cap = ctx->frag_cap = c;
+        }
         PGB_CUDA(cudaSetDevice(device));
         PGB_CUDA(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
         PGB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
@@ -787,6 +924,10 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         ctx->h_counters.release();
         for (auto e : ctx->seg_events) cudaEventDestroy(e);
         for (auto e : ctx->sub_events) cudaEventDestroy(e);
+        for (auto& b : ctx->stage) b.release();
+        for (auto e : ctx->file_dd_ev) cudaEventDestroy(e);
+        ctx->h_file_status.release();
+        ctx->h_file_ctr.release();
         for (int k = 0; k < 2; ++k)
             for (cudaEvent_t e : {ctx->ev_dd0[k], ctx->ev_dd1[k], ctx->ev_front[k], ctx->ev_rms[k]})
                 cudaEventDestroy(e);
@@ -925,6 +1066,7 @@ static pgb_status dedisperse_impl(pgb_context* ctx, const void* data, bool u8, u
                       "trial " + std::to_string(t) + ": chunk of " + std::to_string(length) +
                           " samples cannot cover delay span " + std::to_string(ctx->maxd[t]));
         if (tb == te) return;
+        stage_reset(ctx);
         const uint32_t save_b = ctx->tr_begin, save_e = ctx->tr_end;
         ctx->tr_begin = tb;
         ctx->tr_end = te;
@@ -1115,6 +1257,8 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
             }
         }
         ctx->file_skipped.clear();
+        ctx->trace = getenv("PGB_TRACE") != nullptr;
+        trace_mark(ctx, "begin", ctx->st);
         uint64_t total = 0;
         // back half of a chunk: append its sorted candidates and skipped trials
         auto finish = [&](ChunkRun& run) {
@@ -1150,40 +1294,126 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
         uint64_t pitch_min = 0;  // one series pitch for the whole file (overlap reuse)
         for (size_t k = 0; k < nchunks; ++k) pitch_min = std::max<uint64_t>(pitch_min, chunks[k].length);
         ctx->ser_ok = false;
-        ChunkRun runs[2];
-        bool pending = false;
-        for (size_t k = 0; k < nchunks; ++k) {
-            validate_cfg(ctx, &chunks[k], cfg);
-            const bool prog_k = k == 0 && !payload_on_device && !ctx->prog.empty();
-            if (!payload_on_device && !prog_k) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
-            const uint8_t* cptr = dpay + chunks[k].start_sample * C;
-            ChunkInput ci{cptr, true};
-            ci.raw = true;
-            ci.pitch_min = pitch_min;
-            ci.more = overlap && k + 1 < nchunks;
-            if (prog_k) ci.prog = &ctx->prog;
-            if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
-                uint64_t nbc = 0, nbs = 0;
-                ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);
-                rfi_clean_impl<uint8_t>(cptr, chunks[k].length, C, to_rfi(rfi), ctx->rfi, ctx->rfi_out.as<float>(),
-                                        ctx->st, &nbc, &nbs);
-                ctx->launches += 8;
-                if (nbc || nbs) {
-                    ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
-                    ci.pitch_min = pitch_min;
-                    ci.more = overlap && k + 1 < nchunks;
+        // Back halves: asynchronous (device-side counts, one read at the end of the file)
+        // unless PGB_SYNC_BACK is set (per-chunk host reads, the run_dm_loop path).
+        const bool async_back = !getenv("PGB_SYNC_BACK");
+        uint32_t max_rows = 0;
+        for (uint32_t t = ctx->tr_begin; t < ctx->tr_end; ++t) ++max_rows;
+        struct ChunkBook {  // what the end-of-file pass needs from each chunk
+            bool live = false;
+            uint64_t index = 0;
+            std::vector<uint32_t> active;
+            std::vector<uint64_t> skipped;
+        };
+        std::vector<ChunkBook> book;
+        uint64_t file_cap = 0;
+        auto run_chunks = [&]() {
+            ChunkRun runs[2];
+            bool pending = false;
+            ctx->ser_ok = false;
+            if (async_back) {
+                book.assign(nchunks, ChunkBook{});
+                file_cap = std::max<uint64_t>(1, nchunks * ctx->cand_cap);
+                ctx->file_cands.reserve(file_cap * sizeof(pgb_candidate));
+                ctx->file_ctr.reserve(4 * sizeof(unsigned long long));
+                PGB_CUDA(cudaMemsetAsync(ctx->file_ctr.p, 0, 4 * sizeof(unsigned long long), ctx->st));
+                ctx->h_file_status.reserve(std::max<size_t>(1, nchunks * (size_t)max_rows));
+                ctx->h_file_ctr.reserve(4 * sizeof(unsigned long long));
+                while (ctx->file_dd_ev.size() < 2 * nchunks) {
+                    cudaEvent_t e;
+                    PGB_CUDA(cudaEventCreate(&e));
+                    ctx->file_dd_ev.push_back(e);
                 }
             }
-            ChunkRun& cur = runs[k & 1];
-            chunk_front(ctx, ci, &chunks[k], cfg, (int)(k & 1), cur);
-            if (pending) finish(runs[(k - 1) & 1]);
-            pending = true;
-            if (!overlap) {
-                finish(cur);
-                pending = false;
+            size_t back_k = 0;  // chunk index of the next back half
+            auto back = [&](ChunkRun& run) {
+                if (!async_back) {
+                    finish(run);
+                } else {
+                    ChunkBook& b = book[back_k];
+                    b.live = run.live;
+                    b.index = run.spec.index;
+                    b.active = run.active;
+                    b.skipped = run.skipped;
+                    chunk_back_async(ctx, run, ctx->h_file_status.as<uint8_t>() + back_k * (size_t)max_rows,
+                                     file_cap);
+                }
+                ++back_k;
+            };
+            for (size_t k = 0; k < nchunks; ++k) {
+                validate_cfg(ctx, &chunks[k], cfg);
+                const bool prog_k = k == 0 && !payload_on_device && !ctx->prog.empty();
+                if (!payload_on_device && !prog_k) PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->seg_events[k], 0));
+                const uint8_t* cptr = dpay + chunks[k].start_sample * C;
+                ChunkInput ci{cptr, true};
+                ci.raw = true;
+                ci.pitch_min = pitch_min;
+                ci.more = overlap && k + 1 < nchunks;
+                if (prog_k) ci.prog = &ctx->prog;
+                if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
+                    uint64_t nbc = 0, nbs = 0;
+                    ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);
+                    rfi_clean_impl<uint8_t>(cptr, chunks[k].length, C, to_rfi(rfi), ctx->rfi, ctx->rfi_out.as<float>(),
+                                            ctx->st, &nbc, &nbs);
+                    ctx->launches += 8;
+                    if (nbc || nbs) {
+                        ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
+                        ci.pitch_min = pitch_min;
+                        ci.more = overlap && k + 1 < nchunks;
+                    }
+                }
+                if (async_back) {
+                    ci.ev0 = ctx->file_dd_ev[2 * k];
+                    ci.ev1 = ctx->file_dd_ev[2 * k + 1];
+                }
+                ChunkRun& cur = runs[k & 1];
+                chunk_front(ctx, ci, &chunks[k], cfg, (int)(k & 1), cur);
+                if (pending) back(runs[(k - 1) & 1]);
+                pending = true;
+                if (!overlap) {
+                    back(cur);
+                    pending = false;
+                }
+            }
+            if (pending) back(runs[(nchunks - 1) & 1]);
+        };
+        if (!async_back) {
+            run_chunks();
+        } else {
+            for (;;) {
+                run_chunks();
+                auto* hc = ctx->h_file_ctr.as<unsigned long long>();
+                PGB_CUDA(cudaMemcpyAsync(hc, ctx->file_ctr.p, 3 * sizeof(unsigned long long),
+                                         cudaMemcpyDeviceToHost, ctx->st));
+                PGB_CUDA(cudaStreamSynchronize(ctx->st));
+                total = hc[0];
+                const uint64_t hi_c = hc[1], hi_f = hc[2];
+                if (hi_c <= ctx->cand_cap && hi_f <= ctx->frag_cap && total <= file_cap) break;
+                // a counter overflowed: grow and search the file again (rare)
+                ctx->cand_cap = std::max<uint64_t>(ctx->cand_cap, round_up(hi_c * 2, 1024));
+                ctx->frag_cap = std::max<uint64_t>(ctx->frag_cap, round_up(hi_f * 2, 1024));
+                reset_timing(ctx);
+            }
+            const uint8_t* hs = ctx->h_file_status.as<uint8_t>();
+            for (size_t k = 0; k < nchunks; ++k) {
+                ChunkBook& b = book[k];
+                std::vector<uint64_t> sk = b.skipped;
+                if (b.live)
+                    for (size_t r = 0; r < b.active.size(); ++r)
+                        if (hs[k * (size_t)max_rows + r]) sk.push_back(b.active[r]);
+                std::sort(sk.begin(), sk.end());
+                for (uint64_t t : sk) {
+                    ctx->file_skipped.push_back(b.index);
+                    ctx->file_skipped.push_back(t);
+                }
+                if (b.live) {
+                    float ms = 0.f;
+                    PGB_CUDA(cudaEventElapsedTime(&ms, ctx->file_dd_ev[2 * k], ctx->file_dd_ev[2 * k + 1]));
+                    ctx->dedisp_ms += ms;
+                }
             }
         }
-        if (pending) finish(runs[(nchunks - 1) & 1]);
+        trace_mark(ctx, "chunks done (host sync)", ctx->st);
         // file-level sort (src/pipeline.cpp:100-105) and link_grid (:106)
         ctx->file_sorted.reserve(std::max<uint64_t>(total, 1) * sizeof(pgb_candidate));
         if (total) {
@@ -1201,6 +1431,8 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
             cluster_candidates(ctx->file_sorted.as<pgb_candidate>(), total, *radii, ctx->cl_scratch,
                                ctx->clusters, ctx->members, &ncl, ctx->st, &ctx->launches);
         PGB_CUDA(cudaStreamSynchronize(ctx->st));
+        trace_mark(ctx, "file sort + link_grid", ctx->st);
+        trace_dump(ctx);
         ctx->file_ncands = total;
         ctx->n_clusters = ncl;
         ctx->n_members = radii ? total : 0;

@@ -541,7 +541,9 @@ __global__ void __launch_bounds__(BX_THREADS)
 }
 
 __global__ void stitch_kernel(const Fragment* __restrict__ f, uint64_t nf,
-                              const uint32_t* __restrict__ row_len, PeakCtx ctx) {
+                              const uint32_t* __restrict__ row_len, PeakCtx ctx,
+                              const unsigned long long* __restrict__ d_nf) {
+    if (d_nf) nf = *d_nf < nf ? *d_nf : nf;  // device count, capped at the buffer (nf = cap)
     const uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= nf) return;
     const Fragment a = f[idx];
@@ -651,7 +653,18 @@ void launch_stitch(const Fragment* frags_sorted, uint64_t nfrags, const uint32_t
     if (!nfrags) return;
     PeakCtx ctx{active, dms, cp, cands, n_cands, cand_cap, nullptr, nullptr, 0};
     stitch_kernel<<<(unsigned)((nfrags + 255) / 256), 256, 0, st>>>(frags_sorted, nfrags, row_len,
-                                                                   ctx);
+                                                                   ctx, nullptr);
+    PGB_CUDA(cudaGetLastError());
+}
+
+void launch_stitch_dev(const Fragment* frags_sorted, uint64_t frag_cap, const unsigned long long* d_nf,
+                       const uint32_t* row_len, const ChainParams& cp, const uint32_t* active,
+                       const double* dms, pgb_candidate* cands, unsigned long long* n_cands,
+                       uint64_t cand_cap, cudaStream_t st) {
+    if (!frag_cap) return;
+    PeakCtx ctx{active, dms, cp, cands, n_cands, cand_cap, nullptr, nullptr, 0};
+    stitch_kernel<<<(unsigned)((frag_cap + 255) / 256), 256, 0, st>>>(frags_sorted, frag_cap, row_len,
+                                                                     ctx, d_nf);
     PGB_CUDA(cudaGetLastError());
 }
 

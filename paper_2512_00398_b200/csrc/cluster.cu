@@ -205,6 +205,9 @@ __global__ void __launch_bounds__(1024)
     __shared__ uint32_t parent[LINK_SMEM_MAX];
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) parent[i] = i;
     __syncthreads();
+    // one thread per candidate.  In a dense group (a bright pulse: hundreds of mutually
+    // linked candidates) most pairs are already in one set, so the root comparison comes
+    // first and the candidate record is only read for pairs in different sets.
     for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
         const pgb_candidate a = c[i];
         const int64_t kt = (int64_t)(a.peak_sample / g.cell_t());
@@ -220,7 +223,78 @@ __global__ void __launch_bounds__(1024)
                     uint64_t p = lower_bound(skeys, n, key);
                     for (; p < n && skeys[p] == key; ++p) {
                         const uint32_t j = sidx[p];
-                        if (j > i && linked(a, c[j], g.r)) suf_unite(parent, i, j);
+                        if (j <= i || suf_find(parent, i) == suf_find(parent, j)) continue;
+                        if (linked(a, c[j], g.r)) suf_unite(parent, i, j);
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) parent_out[i] = suf_find(parent, i);
+}
+
+// Up to LINK_SMEM2_MAX candidates: everything the linking reads -- the link fields, the
+// sorted cell keys and indices, the forest -- is staged in shared memory (40 B per
+// candidate), so the serial per-candidate cell walks (hundreds of members for a bright
+// pulse) run at shared-memory latency instead of L1/L2 latency.
+constexpr uint32_t LINK_SMEM2_MAX = 5120;
+
+__global__ void __launch_bounds__(1024)
+    link_smem2_kernel(const pgb_candidate* __restrict__ c, uint32_t n, CellGeom g,
+                      const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx,
+                      uint32_t* parent_out) {
+    extern __shared__ __align__(16) unsigned char lsm[];
+    uint64_t* s_peak = reinterpret_cast<uint64_t*>(lsm);
+    uint64_t* s_ws = s_peak + n;
+    uint64_t* s_key = s_ws + n;
+    uint32_t* s_trial = reinterpret_cast<uint32_t*>(s_key + n);
+    uint32_t* s_widx = s_trial + n;
+    uint32_t* s_sidx = s_widx + n;
+    uint32_t* parent = s_sidx + n;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const pgb_candidate a = c[i];
+        s_peak[i] = a.peak_sample;
+        s_ws[i] = a.width_samples;
+        s_trial[i] = a.dm_trial;
+        s_widx[i] = a.width_index;
+        s_key[i] = skeys[i];
+        s_sidx[i] = sidx[i];
+        parent[i] = i;
+    }
+    __syncthreads();
+    const uint64_t ct = g.cell_t();
+    const uint32_t cd = g.cell_dm(), cw = g.cell_w();
+    const Radii r = g.r;
+    for (uint32_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint64_t pi = s_peak[i], wi = s_ws[i];
+        const uint32_t ti = s_trial[i], xi = s_widx[i];
+        const int64_t kt = (int64_t)(pi / ct), kd = (int64_t)(ti / cd), kw = (int64_t)(xi / cw);
+        for (int64_t dt = -1; dt <= 1; ++dt) {
+            if (kt + dt < 0) continue;
+            for (int64_t dd = -1; dd <= 1; ++dd) {
+                if (kd + dd < 0) continue;
+                for (int64_t dw = -1; dw <= 1; ++dw) {
+                    if (kw + dw < 0) continue;
+                    const uint64_t key = cell_key(kt + dt, kd + dd, kw + dw);
+                    uint32_t lo = 0, hi = n;
+                    while (lo < hi) {
+                        const uint32_t mid = (lo + hi) >> 1;
+                        if (s_key[mid] < key) lo = mid + 1;
+                        else hi = mid;
+                    }
+                    for (uint32_t p = lo; p < n && s_key[p] == key; ++p) {
+                        const uint32_t j = s_sidx[p];
+                        if (j <= i || suf_find(parent, i) == suf_find(parent, j)) continue;
+                        // linked() on the staged fields (src/cluster.cpp:77-88)
+                        const uint64_t pj = s_peak[j];
+                        const uint64_t dtm = pi > pj ? pi - pj : pj - pi;
+                        const uint64_t wm = wi > s_ws[j] ? wi : s_ws[j];
+                        if (dtm > r.sep_time * wm) continue;
+                        const uint32_t tj = s_trial[j], xj = s_widx[j];
+                        if ((ti > tj ? ti - tj : tj - ti) > r.sep_dm) continue;
+                        if ((xi > xj ? xi - xj : xj - xi) > r.sep_w) continue;
+                        suf_unite(parent, i, j);
                     }
                 }
             }
@@ -380,7 +454,17 @@ void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_r
     cub::DoubleBuffer<uint64_t> ck(keys_a, keys_b);
     cub::DoubleBuffer<uint32_t> cv(idx_a, idx_b);
     PGB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, sort_tmp, ck, cv, (int)n, 0, 64, st));
-    if (n <= LINK_SMEM_MAX && !getenv("PGB_LINK_GLOBAL"))
+    const int link_mode = [] {  // ablation: PGB_LINK_GLOBAL=1 / PGB_LINK_SMEM1=1
+        if (getenv("PGB_LINK_GLOBAL")) return 2;
+        if (getenv("PGB_LINK_SMEM1")) return 1;
+        return 0;
+    }();
+    if (n <= LINK_SMEM2_MAX && link_mode == 0) {
+        const size_t smem = (size_t)40 * n;
+        PGB_CUDA(cudaFuncSetAttribute(link_smem2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                      (int)(40 * LINK_SMEM2_MAX)));
+        link_smem2_kernel<<<1, 1024, smem, st>>>(cands, (uint32_t)n, g, ck.Current(), cv.Current(), parent);
+    } else if (n <= LINK_SMEM_MAX && link_mode != 2)
         link_smem_kernel<<<1, 1024, 0, st>>>(cands, (uint32_t)n, g, ck.Current(), cv.Current(), parent);
     else
         link_kernel<<<nblk(n), 256, 0, st>>>(cands, n, g, ck.Current(), cv.Current(), parent);

@@ -154,6 +154,29 @@ void launch_stitch(const Fragment* frags_sorted, uint64_t nfrags, const uint32_t
                    pgb_candidate* cands, unsigned long long* n_cands, uint64_t cand_cap,
                    cudaStream_t st);
 
+// device-count variants (file search, no host round trip per chunk): d_n is the emission
+// counter (may exceed cap on overflow); cap items are sorted
+void sort_fragments_dev(Fragment* frags, Fragment* out, uint64_t cap, const unsigned long long* d_n,
+                        void* temp, size_t temp_bytes, uint64_t* keys_a, uint64_t* keys_b,
+                        uint32_t* idx_a, uint32_t* idx_b, cudaStream_t st);
+void sort_candidates_dev(const pgb_candidate* in, pgb_candidate* out, uint64_t cap,
+                         const unsigned long long* d_n, void* temp, size_t temp_bytes,
+                         uint64_t* keys_a, uint64_t* keys_b, uint32_t* idx_a, uint32_t* idx_b,
+                         cudaStream_t st);
+// file_cands[total ..) += sorted[0 .. min(count, cap)); total += that; d_counts = {nc, nf},
+// d_hiwater = running max of both (overflow check at the end of the file)
+void append_candidates_dev(const pgb_candidate* sorted, uint64_t cap, const unsigned long long* d_counts,
+                           pgb_candidate* file_cands, unsigned long long* d_total, uint64_t file_cap,
+                           unsigned long long* d_hiwater, cudaStream_t st);
+void launch_stitch_dev(const Fragment* frags_sorted, uint64_t frag_cap, const unsigned long long* d_nf,
+                       const uint32_t* row_len, const ChainParams& cp, const uint32_t* active,
+                       const double* dms, pgb_candidate* cands, unsigned long long* n_cands,
+                       uint64_t cand_cap, cudaStream_t st);
+
+// dst (device) = bytes read by a kernel from pinned host memory (no copy engine); bytes is
+// rounded up to whole 32-bit words
+void launch_copy_from_host(void* dst, const void* pinned_src, size_t bytes, cudaStream_t st);
+
 // sorting helpers (CUB)
 size_t sort_fragments_temp_bytes(uint64_t n);
 void sort_fragments(Fragment* frags, Fragment* tmp, uint64_t n, void* temp, size_t temp_bytes,

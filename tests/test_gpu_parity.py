@@ -244,19 +244,20 @@ def test_link_grid_vs_reference_library(engine, ref):
     clusters_equal(got, recs, members)
 
 
-@pytest.mark.parametrize("n,extent", [(3000, 20_000), (12288, 2_000_000), (20000, 3_000_000)])
+@pytest.mark.parametrize("n,extent", [(3000, 20_000), (5120, 200_000), (12288, 2_000_000),
+                                      (20000, 3_000_000)])
 def test_link_grid_smem_and_global_forests_agree(engine, port, monkeypatch, n, extent):
-    """link_grid links sets of <= 12288 candidates with a shared-memory union-find and
-    larger ones with the global one; both must give the reference clusters (dense sets
-    make big components and contended unions)."""
+    """link_grid links sets of <= 5120 candidates with everything staged in shared memory,
+    <= 12288 with a shared-memory forest and larger ones with the global one; every variant
+    must give the reference clusters (dense sets make big components and contended unions)."""
     rng = np.random.default_rng(n)
     cands = random_candidates(rng, n, extent)
-    a = engine.link_grid(cands, LinkRadii())
-    monkeypatch.setenv("PGB_LINK_GLOBAL", "1")
-    b = engine.link_grid(cands, LinkRadii())
     recs, members = port.link_grid(cands, (3, 9, 3))
-    clusters_equal(a, recs, members)
-    clusters_equal(b, recs, members)
+    clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)
+    monkeypatch.setenv("PGB_LINK_SMEM1", "1")
+    clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)
+    monkeypatch.setenv("PGB_LINK_GLOBAL", "1")
+    clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)
 
 
 def test_link_grid_ties(engine):

@@ -63,3 +63,32 @@ def test_progressive_first_chunk_matches(monkeypatch):
         for k in a.candidates.dtype.names:
             assert np.array_equal(a.candidates[k], other.candidates[k]), k
         assert write_candidates(other.clusters) == write_candidates(a.clusters)
+
+
+@pytest.mark.parametrize("initial_cap", [None, "64"])
+def test_async_back_halves_match_sync(monkeypatch, initial_cap):
+    """The file search's back halves run without host round trips (device-side counts,
+    one read per file); the result must equal the per-chunk synchronous path
+    (PGB_SYNC_BACK=1), also when tiny initial buffers force the overflow-and-retry path."""
+    from paper_2512_00398_b200.engine import Engine
+
+    hdr = FilterbankHeader(fch1=1500.0, foff=-1.0, nchans=256, tsamp=64e-6, nsamples=3 << 15)
+    params = SearchParams(dm_lo=0.0, dm_hi=300.0, spacing=LinearSpacing(2.0),
+                          engine=EngineConfig(boxcar_max=1024), baseline_len_s=0.25,
+                          nsamps_chunk=1 << 15, rfi=RfiConfig(False, False))
+    task = create_task(hdr, params)
+    payload = u8_chunk(hdr, task.plan, hdr.nsamples, seed=79,
+                       pulses=[(30, 9000, 4, 25.0), (100, 40000, 512, 40.0), (140, 70000, 64, 30.0)])
+    if initial_cap:
+        monkeypatch.setenv("PGB_INITIAL_CAP", initial_cap)
+    res = []
+    for sync in (False, True):
+        if sync:
+            monkeypatch.setenv("PGB_SYNC_BACK", "1")
+        with Engine(0) as eng:
+            res.append(eng.search_file(payload, hdr.nsamples, task.chunks, task.plan, task.engine))
+    (a, ca, sa), (b, cb, sb) = res
+    assert len(a) == len(b) > 0
+    for k in a.dtype.names:
+        assert np.array_equal(a[k], b[k]), k
+    assert np.array_equal(ca.records, cb.records) and np.array_equal(sa, sb)
