@@ -248,7 +248,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     import torch
 
     from paper_2512_00398_b200 import _native
-    from paper_2512_00398_b200.distributed import gather_candidates, shard_trials, trial_work
+    from paper_2512_00398_b200.distributed import DD_TRIAL_BLOCK, gather_candidates, shard_trials, trial_work
     from paper_2512_00398_b200.engine import Engine
 
     # PG_DIST_BACKEND=gloo + PG_SAME_GPU=1 exercise the multi-rank path on one GPU
@@ -272,7 +272,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     torch.cuda.synchronize()
     log(f"[rank {rank}] payload {tuple(payload.shape)} generated in {time.time() - t0:.1f}s; "
         f"{len(task.chunks)} chunks, {plan.ntrials} trials, baseline window {task.engine.baseline_window}")
-    lo, hi = shard_trials(trial_work(plan, [c.length for c in task.chunks]), world)[rank]
+    lo, hi = shard_trials(trial_work(plan, [c.length for c in task.chunks]), world, DD_TRIAL_BLOCK)[rank]
     eng = Engine(local_rank)
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{local_rank}")
     dev = torch.device("cuda", local_rank)

@@ -25,12 +25,25 @@ def trial_work(plan, chunk_lengths) -> np.ndarray:
     return w * plan.nchans
 
 
-def shard_trials(work: np.ndarray, world: int) -> list[tuple[int, int]]:
+DD_TRIAL_BLOCK = 32  # trials per dedispersion CTA (csrc: 16 warps x 2 trials)
+
+
+def shard_trials(work: np.ndarray, world: int, granule: int = 1) -> list[tuple[int, int]]:
     """Contiguous trial ranges with (near-)equal total work; every range non-empty
-    when ntrials >= world."""
+    when ntrials >= world.
+
+    granule > 1 (the dedispersion kernel's 32-trial block): ranges start on multiples of
+    `granule` and a block costs `granule` x its longest trial's work -- a block with
+    fewer trials takes as long as a full one, so a shard of 119 trials (3 full blocks
+    + 23) would pay 7 % for the partial block."""
     n = len(work)
     if world <= 1 or n == 0:
         return [(0, n)] + [(n, n)] * max(0, world - 1)
+    if granule > 1 and n >= granule * world:
+        nb = (n + granule - 1) // granule
+        bcost = np.array([granule * work[b * granule:(b + 1) * granule].max() for b in range(nb)])
+        inner = shard_trials(bcost, world, 1)
+        return [(lo * granule, min(n, hi * granule)) for lo, hi in inner]
     cum = np.concatenate([[0.0], np.cumsum(work)])
     total = cum[-1]
     bounds = [0]
@@ -94,7 +107,7 @@ def search_file_distributed(payload, task, *, rank: int, world: int, device: int
     from .pipeline import SearchResult
 
     work = trial_work(task.plan, [c.length for c in task.chunks])
-    lo, hi = shard_trials(work, world)[rank]
+    lo, hi = shard_trials(work, world, DD_TRIAL_BLOCK)[rank]
     eng = default_engine(device)
     cands, _, skipped = eng.search_file(payload, task.header.nsamples, task.chunks, task.plan,
                                         task.engine, trial_range=(lo, hi), cluster=False)

@@ -85,3 +85,18 @@ def test_gather_reproduces_single_device_order(world):
     assert len(got) == len(want)
     for k in abi.CANDIDATE_DTYPE.names:  # field by field (padding bytes are unspecified)
         assert np.array_equal(got[k], want[k]), k
+
+
+def test_shard_trials_block_granule():
+    """Shards on 32-trial dedispersion blocks: every boundary a multiple of 32, all trials
+    covered once, block-cost balance within one block."""
+    rng = np.random.default_rng(1)
+    w = np.sort(rng.uniform(5, 10, 1001))[::-1].copy()  # work falls with DM
+    for world in (2, 4, 8):
+        shards = shard_trials(w, world, 32)
+        assert shards[0][0] == 0 and shards[-1][1] == 1001
+        assert all(a[1] == b[0] for a, b in zip(shards, shards[1:]))
+        assert all(lo % 32 == 0 and hi > lo for lo, hi in shards)
+        cost = [32 * sum(w[b:b + 32].max() for b in range(lo, hi, 32)) for lo, hi in shards]
+        assert max(cost) - min(cost) <= 2 * 32 * w.max()
+    assert shard_trials(w[:40], 4, 32) == shard_trials(w[:40], 4)  # too few blocks: plain split

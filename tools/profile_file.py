@@ -9,7 +9,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_2512_00398_b200.distributed import shard_trials, trial_work  # noqa: E402
+from paper_2512_00398_b200.distributed import DD_TRIAL_BLOCK, shard_trials, trial_work  # noqa: E402
 from paper_2512_00398_b200.engine import Engine  # noqa: E402
 
 world = int(sys.argv[1]) if len(sys.argv) > 1 else 1
@@ -19,7 +19,7 @@ cfg = dict(bench.CONFIG_B)
 task = bench.build_task(cfg)
 payload = bench.make_payload(cfg, task.plan)
 torch.cuda.synchronize()
-lo, hi = shard_trials(trial_work(task.plan, [c.length for c in task.chunks]), world)[rank]
+lo, hi = shard_trials(trial_work(task.plan, [c.length for c in task.chunks]), world, DD_TRIAL_BLOCK)[rank]
 with Engine(0) as eng:
     for _ in range(reps - 1):
         eng.search_file(payload, cfg["nsamples"], task.chunks, task.plan, task.engine,

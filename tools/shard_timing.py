@@ -15,7 +15,7 @@ sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
 import torch  # noqa: E402
 
 import bench  # noqa: E402
-from paper_2512_00398_b200.distributed import shard_trials, trial_work  # noqa: E402
+from paper_2512_00398_b200.distributed import DD_TRIAL_BLOCK, shard_trials, trial_work  # noqa: E402
 from paper_2512_00398_b200.engine import Engine  # noqa: E402
 
 ap = argparse.ArgumentParser()
@@ -32,7 +32,7 @@ with Engine(0) as eng:
     stream = torch.cuda.ExternalStream(eng.stream_handle(), device="cuda:0")
     for world in (1, 2, 4, 8):
         worst = 0.0
-        for rank, (lo, hi) in enumerate(shard_trials(work, world)):
+        for rank, (lo, hi) in enumerate(shard_trials(work, world, DD_TRIAL_BLOCK)):
             def run():
                 return eng.search_file(payload, cfg["nsamples"], task.chunks, plan, task.engine,
                                        trial_range=(lo, hi), cluster=(world == 1))
