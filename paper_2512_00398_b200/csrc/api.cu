@@ -747,13 +747,13 @@ void chunk_back_async(pgb_context* ctx, ChunkRun& run, uint8_t* h_status, uint64
     launch_stitch_dev(ctx->frags_sorted.as<Fragment>(), fcap, dcnt + 1, ctx->d_row_len[slot].as<uint32_t>(),
                       cp, ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
                       ctx->cands_raw.as<pgb_candidate>(), dcnt, ccap, st);
-    sort_candidates_dev(ctx->cands_raw.as<pgb_candidate>(), ctx->cands_sorted.as<pgb_candidate>(), ccap,
-                        dcnt, ctx->sort_tmp.p, tmp, ka, ka + cap, ia, ia + cap, st);
+    // no per-chunk candidate order: the file-level sort (src/pipeline.cpp:100-105) orders
+    // the appended candidates of all chunks by the same unique key
     auto* fc = ctx->file_ctr.as<unsigned long long>();
-    append_candidates_dev(ctx->cands_sorted.as<pgb_candidate>(), ccap, dcnt,
+    append_candidates_dev(ctx->cands_raw.as<pgb_candidate>(), ccap, dcnt,
                           ctx->file_cands.as<pgb_candidate>(), fc, file_cap, fc + 1, st);
     PGB_CUDA(cudaMemcpyAsync(h_status, ctx->status[slot].p, run.nrows, cudaMemcpyDeviceToHost, st));
-    trace_mark(ctx, "fragment/candidate order + append", st);
+    trace_mark(ctx, "fragment order + stitch + append", st);
     ctx->launches += 12;
 }
 

@@ -817,38 +817,56 @@ __global__ void series_shift_kernel(int32_t* __restrict__ series, uint64_t pitch
 
 // ---- transposes ---------------------------------------------------------------
 
-// u8 [length][nchans] -> rows [nchans][pitch]; 64x64-byte tiles.
-__global__ void transpose_u8_kernel(const uint8_t* __restrict__ in, uint64_t length,
-                                    uint32_t nchans, uint8_t* __restrict__ rows, uint64_t pitch) {
-    __shared__ uint8_t tile[64][64 + 4];
-    const uint64_t t0 = (uint64_t)blockIdx.x * 64;
+// u8 [length][nchans] -> rows [nchans][pitch]; tiles of TT samples x 64 channels, 256
+// threads, TT/64 16-byte loads and stores per thread (TT = 256 keeps 16 KB per CTA in
+// flight: the 64 x 64 tile left the copy at ~55 % of HBM bandwidth, latency-bound on
+// bytes in flight).
+template <int TT>
+__global__ void __launch_bounds__(256) transpose_u8_kernel(const uint8_t* __restrict__ in, uint64_t length,
+                                                            uint32_t nchans, uint8_t* __restrict__ rows,
+                                                            uint64_t pitch) {
+    constexpr int R = TT / 64;  // rows (and output vectors) per thread
+    __shared__ uint8_t tile[TT][64 + 4];
+    const uint64_t t0 = (uint64_t)blockIdx.x * TT;
     const uint32_t c0 = blockIdx.y * 64;
     const int tid = threadIdx.x;
-    const bool full = (t0 + 64 <= length) && (c0 + 64 <= nchans) && (nchans % 16 == 0);
+    const bool full = (t0 + TT <= length) && (c0 + 64 <= nchans) && (nchans % 16 == 0);
     if (full) {
-        const int r = tid >> 2, cv = (tid & 3) * 16;
-        const uint4 v = __ldg(reinterpret_cast<const uint4*>(in + (t0 + r) * nchans + c0 + cv));
-        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        const int cv = (tid & 3) * 16;
+        uint4 v[R];
 #pragma unroll
-        for (int k = 0; k < 4; ++k) *reinterpret_cast<uint32_t*>(&tile[r][cv + 4 * k]) = w[k];
+        for (int k = 0; k < R; ++k)
+            v[k] = __ldg(reinterpret_cast<const uint4*>(in + (t0 + (tid >> 2) + 64 * k) * nchans + c0 + cv));
+#pragma unroll
+        for (int k = 0; k < R; ++k) {
+            const int r = (tid >> 2) + 64 * k;
+            *reinterpret_cast<uint32_t*>(&tile[r][cv]) = v[k].x;
+            *reinterpret_cast<uint32_t*>(&tile[r][cv + 4]) = v[k].y;
+            *reinterpret_cast<uint32_t*>(&tile[r][cv + 8]) = v[k].z;
+            *reinterpret_cast<uint32_t*>(&tile[r][cv + 12]) = v[k].w;
+        }
     } else {
-        for (int k = tid; k < 64 * 64; k += blockDim.x) {
+        for (int k = tid; k < TT * 64; k += blockDim.x) {
             const int r = k >> 6, c = k & 63;
             tile[r][c] = (t0 + r < length && c0 + c < nchans) ? in[(t0 + r) * nchans + c0 + c] : 0;
         }
     }
     __syncthreads();
-    // write: thread -> (channel c, 16 consecutive samples)
-    const int c = tid >> 2, tv = (tid & 3) * 16;
+    // write: thread -> (channel c, R runs of 16 consecutive samples)
+    const int c = tid >> 2;
     if (c0 + c < nchans) {
-        uint32_t w[4];
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
-            w[k] = (uint32_t)tile[tv + 4 * k][c] | (uint32_t)tile[tv + 4 * k + 1][c] << 8 |
-                   (uint32_t)tile[tv + 4 * k + 2][c] << 16 | (uint32_t)tile[tv + 4 * k + 3][c] << 24;
-        uint8_t* dst = rows + (uint64_t)(c0 + c) * pitch + t0 + tv;
-        if (t0 + tv + 16 <= pitch)
-            *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        for (int k = 0; k < R; ++k) {
+            const int tv = ((tid & 3) + 4 * k) * 16;
+            uint32_t w[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                w[q] = (uint32_t)tile[tv + 4 * q][c] | (uint32_t)tile[tv + 4 * q + 1][c] << 8 |
+                       (uint32_t)tile[tv + 4 * q + 2][c] << 16 | (uint32_t)tile[tv + 4 * q + 3][c] << 24;
+            uint8_t* dst = rows + (uint64_t)(c0 + c) * pitch + t0 + tv;
+            if (t0 + tv + 16 <= pitch)
+                *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+        }
     }
 }
 
@@ -1047,8 +1065,15 @@ void launch_series_shift(int32_t* series, uint32_t nrows, uint64_t pitch, uint64
 
 void launch_transpose_u8(const uint8_t* in, uint64_t length, uint32_t nchans, uint8_t* rows,
                          uint64_t pitch, cudaStream_t st) {
-    dim3 grid((unsigned)((length + 63) / 64), (nchans + 63) / 64);
-    transpose_u8_kernel<<<grid, 256, 0, st>>>(in, length, nchans, rows, pitch);
+    static const int tt = [] {  // PGB_TRANSPOSE_TT: time-tile ablation (64 / 128 / 256)
+        const char* e = getenv("PGB_TRANSPOSE_TT");
+        const int v = e ? atoi(e) : 256;
+        return v == 64 || v == 128 ? v : 256;
+    }();
+    dim3 grid((unsigned)((length + tt - 1) / tt), (nchans + 63) / 64);
+    if (tt == 64) transpose_u8_kernel<64><<<grid, 256, 0, st>>>(in, length, nchans, rows, pitch);
+    else if (tt == 128) transpose_u8_kernel<128><<<grid, 256, 0, st>>>(in, length, nchans, rows, pitch);
+    else transpose_u8_kernel<256><<<grid, 256, 0, st>>>(in, length, nchans, rows, pitch);
     PGB_CUDA(cudaGetLastError());
 }
 
