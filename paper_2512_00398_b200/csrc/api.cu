@@ -121,7 +121,7 @@ struct pgb_context {
     // (transpose, dedispersion, baseline, RMS) to its back half (boxcar, runs, order)
     DevBuf base[2], frms[2], status[2], d_row_len[2], slot_active[2];
     DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
-    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off, d_keep;
+    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off, d_keep, d_work;
     // what the series buffer holds: the dedispersed rows of the raw-sample chunk
     // [ser_start, ser_start + ser_len) at pitch ser_pitch (overlap reuse)
     bool ser_ok = false;
@@ -511,6 +511,15 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                 for (uint32_t r = 0; r < nrows; ++r) reused += (uint64_t)keep[r] * C;
             }
         }
+        // persistent ring kernel: one CTA per SM pulling (block, tile) items from a counter
+        if (!getenv("PGB_DD_PERSIST0")) {
+            ctx->d_work.reserve(64 * sizeof(uint32_t), true);
+            dl.work_ctr = ctx->d_work.as<uint32_t>();
+        }
+        auto dd_launch = [&](const DedispLaunch& part) {
+            if (part.work_ctr) PGB_CUDA(cudaMemsetAsync(part.work_ctr, 0, sizeof(uint32_t), st));
+            launch_dedisp_u8(part, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+        };
         if (progressive && dl.tile0 == 0) {
             // tile t reads channel rows up to t*DD_NT + max delay + DD_NT + 20 bytes (window
             // start rounded down to 16, whole 16-byte vectors, one extra word)
@@ -532,7 +541,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                     DedispLaunch part = dl;
                     part.tile0 = done;
                     part.ntiles = t_end;
-                    launch_dedisp_u8(part, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+                    dd_launch(part);
                     ctx->launches += 1;
                     done = t_end;
                 }
@@ -540,10 +549,10 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
             if (done < ntiles) {  // (the last sub-segment ends at L, so this does not happen)
                 DedispLaunch part = dl;
                 part.tile0 = done;
-                launch_dedisp_u8(part, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+                dd_launch(part);
             }
         } else {
-            launch_dedisp_u8(dl, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
+            dd_launch(dl);
         }
         if (in.raw) {
             ctx->ser_ok = true;
@@ -914,6 +923,9 @@ pgb_status pgb_destroy(pgb_context* ctx) {
             for (DevBuf* b : {&ctx->base[k], &ctx->frms[k], &ctx->status[k], &ctx->d_row_len[k],
                               &ctx->slot_active[k]})
                 b->release();
+        ctx->d_work.release();
+        ctx->d_keep.release();
+        ctx->file_ctr.release();
         for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,
                           &ctx->d_active, &ctx->d_blk_len, &ctx->d_scale, &ctx->in_u8, &ctx->ws_base, &ctx->ws_off, &ctx->dd_win, &ctx->dd_off, &ctx->rfi_out, &ctx->rfi.chan_bad,
                           &ctx->rfi.samp_bad, &ctx->rfi.dbl, &ctx->rfi.tmp, &ctx->rfi.rows, &ctx->cands_raw, &ctx->cands_sorted,

@@ -303,10 +303,11 @@ constexpr int RING_NS = 3;
 // MODE bits (ablation): 1 = byte shifts of the staged copies on the FMA pipe
 // (mul.hi + mad.lo funnel) instead of PRMT on the ALU pipe; 2 = per-(channel, trial)
 // shared-memory addresses formed with IMAD (FMA pipe) instead of IADD (ALU pipe)
+// One (trial block, time tile) of the ring kernel; the whole CTA calls it.
 template <int G, int VPT, int MODE>
-__global__ void __launch_bounds__(DD_THREADS, 1)
-    dedisp_u8_ring_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
-                          int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+__device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* __restrict__ rows,
+                                          int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len,
+                                          const uint32_t blk, const uint32_t tile) {
     constexpr int TPW = 2;
     constexpr int TB = DD_WARPS * TPW;
     static_assert(TB == 32, "table layout assumes 32-trial blocks");
@@ -318,13 +319,9 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     uint64_t* full = reinterpret_cast<uint64_t*>(offs + NS * G * TB);              // [NS]
     uint64_t* empty = full + NS;                                                   // [NS]
 
-    const uint32_t blk = blockIdx.x;
     const uint32_t row0 = blk * TB;
     const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
-    const uint32_t tile = blockIdx.y + p.tile0;
-    if (p.blk_first && tile < p.blk_first[blk]) return;  // shifted in from the previous chunk
     const uint64_t i0 = (uint64_t)tile * DD_NT;
-    if (i0 >= blk_len[blk]) return;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nstages = p.nchans_pad / G;
@@ -502,6 +499,40 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
         ph_prev = ph;
         if (++slot == NS) { slot = 0; ph ^= 1; }
         if (++slot2 == NS) slot2 = 0;
+    }
+}
+
+template <int G, int VPT, int MODE>
+__global__ void __launch_bounds__(DD_THREADS, 1)
+    dedisp_u8_ring_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
+                          int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    const uint32_t blk = blockIdx.x;
+    const uint32_t tile = blockIdx.y + p.tile0;
+    if (p.blk_first && tile < p.blk_first[blk]) return;  // shifted in from the previous chunk
+    if ((uint64_t)tile * DD_NT >= blk_len[blk]) return;
+    ring_tile<G, VPT, MODE>(p, rows, out, blk_len, blk, tile);
+}
+
+// Persistent variant: one CTA per SM takes (block, tile) items from a counter in the
+// grid's order (blocks fastest), so the last wave is not quantised to whole CTAs of a
+// 7-55-wave grid (the tail is ~1 % of a launch with 8192 CTAs, several % with 1024).
+template <int G, int VPT>
+__global__ void __launch_bounds__(DD_THREADS, 1)
+    dedisp_u8_ring_persist_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
+                                  int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    __shared__ uint32_t s_item;
+    const uint32_t nblocks = (p.nrows + 31) / 32;
+    const uint32_t items = nblocks * (p.ntiles - p.tile0);
+    for (;;) {
+        __syncthreads();  // every warp is done with the previous item (and with s_item)
+        if (threadIdx.x == 0) s_item = atomicAdd(p.work_ctr, 1u);
+        __syncthreads();
+        const uint32_t item = s_item;
+        if (item >= items) return;
+        const uint32_t blk = item % nblocks, tile = p.tile0 + item / nblocks;
+        if (p.blk_first && tile < p.blk_first[blk]) continue;
+        if ((uint64_t)tile * DD_NT >= blk_len[blk]) continue;
+        ring_tile<G, VPT, 0>(p, rows, out, blk_len, blk, tile);
     }
 }
 
@@ -928,6 +959,16 @@ size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax) {
     return staged + (size_t)2 * g * tb * 4 + (size_t)2 * g * 8;
 }
 
+int num_sms() {
+    static const int n = [] {
+        int dev = 0, v = 0;
+        PGB_CUDA(cudaGetDevice(&dev));
+        PGB_CUDA(cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev));
+        return v;
+    }();
+    return n;
+}
+
 size_t ring_smem_bytes(int g, uint32_t wmax) {
     return (size_t)RING_NS * g * 4 * wmax + (size_t)RING_NS * g * 32 * 4 + 2 * RING_NS * sizeof(uint64_t);
 }
@@ -973,6 +1014,14 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         // barrier kernel with the larger stage is faster (18.4 vs 19.0 T adds/s on C)
         if (rsm <= 227 * 1024 && g >= p.g) {
 #define PGB_RING3(G_, V_, M_)                                                                     \
+    if (g == G_ && vpt <= V_ && rmode == M_ && M_ == 0 && p.work_ctr) {                           \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_>,                      \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \
+        dedisp_u8_ring_persist_kernel<G_, V_><<<num_sms(), DD_THREADS, rsm, st>>>(p, rows, out,  \
+                                                                                 p.blk_len);      \
+        PGB_CUDA(cudaGetLastError());                                                             \
+        return;                                                                                   \
+    }                                                                                             \
     if (g == G_ && vpt <= V_ && rmode == M_) {                                                    \
         PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_kernel<G_, V_, M_>,                          \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \

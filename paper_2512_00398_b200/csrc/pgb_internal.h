@@ -118,6 +118,7 @@ struct DedispLaunch {
     // chunk's series (shifted in from the previous chunk); grid.y starts at tile0
     const uint32_t* blk_first;  // [nblocks] or null
     uint32_t tile0;
+    uint32_t* work_ctr;         // persistent ring kernel: zeroed item counter (or null)
 };
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st);
 // builds p.dd_win / p.dd_off for the active set (tile independent; p.wmax = bytes per copy)
