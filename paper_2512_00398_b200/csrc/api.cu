@@ -33,8 +33,13 @@ void check_cuda(cudaError_t e, const char* what) {
 
 void DevBuf::reserve(size_t n, bool zero) {
     if (n <= bytes && p) return;
+    // grow geometrically (at least 2x, 64 KB granules): a file search sizes several
+    // buffers by its candidate count, and an exact-size regrowth per file meant a
+    // cudaFree -- a device-wide synchronisation -- in nearly every call (config D's
+    // concurrent contexts stalled each other on it)
+    const size_t grown = p ? std::max<size_t>(n, 2 * bytes) : n;
     release();
-    const size_t want = std::max<size_t>(n, 256);
+    const size_t want = std::max<size_t>((grown + 65535) & ~size_t(65535), 256);
     PGB_CUDA(cudaMalloc(&p, want));
     bytes = want;
     if (zero) PGB_CUDA(cudaMemset(p, 0, want));
@@ -46,9 +51,11 @@ void DevBuf::release() {
 }
 void PinnedBuf::reserve(size_t n) {
     if (n <= bytes && p) return;
+    const size_t grown = p ? std::max<size_t>(n, 2 * bytes) : n;
     release();
-    PGB_CUDA(cudaMallocHost(&p, std::max<size_t>(n, 256)));
-    bytes = std::max<size_t>(n, 256);
+    const size_t want = std::max<size_t>((grown + 4095) & ~size_t(4095), 256);
+    PGB_CUDA(cudaMallocHost(&p, want));
+    bytes = want;
 }
 void PinnedBuf::release() {
     if (p) cudaFreeHost(p);

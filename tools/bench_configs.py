@@ -107,10 +107,11 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["A", "D", "C", "E"])
     ap.add_argument("--steps", type=int, default=2)
+    ap.add_argument("--n-exec", type=int, default=4, help="config D: concurrent device contexts")
     args = ap.parse_args()
     for name in args.configs:
         if name == "D":
-            out = run_multi(args.steps)
+            out = run_multi(args.steps, n_exec=args.n_exec)
         else:
             out = run_file(dict(CONFIGS[name]), args.steps)
         print(json.dumps(out), flush=True)
