@@ -134,6 +134,8 @@ struct pgb_context {
     bool ser_ok = false;
     uint64_t ser_start = 0, ser_len = 0, ser_pitch = 0;
     uint32_t dd_tab_wmax = 0;  // wmax the staging table was built for (0 = stale)
+    DevBuf ddf_win, ddf_off;     // f32 staging table (RFI-masked, non-integer chunks)
+    uint32_t ddf_tab_wmax = 0;
     DevBuf file_cands, file_sorted;
     // asynchronous file-search back halves: {candidate total, high-water nc, nf}, the
     // per-chunk degenerate-trial flags (pinned) and per-chunk dedispersion events
@@ -368,6 +370,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         ctx->active = active;
         ctx->geom_valid = true;
         ctx->dd_tab_wmax = 0;
+        ctx->ddf_tab_wmax = 0;
         ctx->d_active.reserve(nrows * sizeof(uint32_t));
         stage_h2d(ctx, ctx->d_active.p, active.data(), nrows * sizeof(uint32_t), st);
     }
@@ -568,7 +571,21 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
             ctx->ser_pitch = out_pitch;
         }
     }
-    else launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
+    else {
+        dl.nchans_pad = (C + 7) & ~7u;
+        if (dl.tpw == 2) {
+            if (ctx->ddf_tab_wmax != wmax) {
+                ctx->ddf_win.reserve((size_t)nblocks * dl.nchans_pad * sizeof(uint2));
+                ctx->ddf_off.reserve((size_t)nblocks * dl.nchans_pad * 32 * 4);
+                launch_ddf_table(dl, ctx->ddf_win.as<uint2>(), ctx->ddf_off.as<uint32_t>(), st);
+                ctx->launches += 1;
+                ctx->ddf_tab_wmax = wmax;
+            }
+            dl.dd_win = ctx->ddf_win.as<uint2>();
+            dl.dd_off = ctx->ddf_off.as<uint32_t>();
+        }
+        launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
+    }
     PGB_CUDA(cudaEventRecord(in.ev1 ? in.ev1 : ctx->ev_dd1[slot], st));
     trace_mark(ctx, "dedispersion", st);
     ctx->dedisp_launches += 1;

@@ -836,6 +836,138 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     }
 }
 
+// ---- f32 ring (non-integer chunks) ------------------------------------------------
+// Table for the f32 kernels, one warp per (trial block, channel): window start
+// i0 + (min delay & ~3) (16-byte aligned) and its length in float4 vectors; per trial the
+// float offset into the channel's window.  Channels past nchans get empty windows.
+__global__ void ddf_table_kernel(const DedispLaunch p, uint2* __restrict__ win, uint32_t* __restrict__ off) {
+    const uint32_t gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const uint32_t blk = gw / p.nchans_pad, c = gw % p.nchans_pad;
+    const uint32_t nblocks = (p.nrows + 31) / 32;
+    if (blk >= nblocks) return;
+    const uint32_t row0 = blk * 32, nrows_blk = min(32u, p.nrows - row0);
+    const uint32_t row = row0 + min((uint32_t)lane, nrows_blk - 1);
+    const bool live = c < p.nchans;
+    const uint32_t d = live ? (uint32_t)__ldg(p.delays_ct + (size_t)c * p.ntrials_plan + p.active[row]) : 0;
+    const uint32_t dmin = warp_min_u32(d), dmax = warp_max_u32(d);
+    const uint32_t a = dmin & ~3u;
+    off[(size_t)gw * 32 + lane] = d - a;
+    if (lane == 0) win[gw] = make_uint2(a, live ? (dmax - a + DD_NT + 3) / 4 : 0);
+}
+
+// Same channel-ordered IEEE fp32 sums as dedisp_f32_kernel, staged through a 4-slot
+// ring filled by cp.async: every thread's copies of a stage arrive on the slot's `full`
+// mbarrier when they land (cp.async.mbarrier.arrive.noinc), warps arrive on `empty`
+// after adding a stage, and a stage is issued three stages ahead.  No CTA barrier and no
+// staging registers.
+constexpr int FRING_NS = 4;
+
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(sh_addr(bar)) : "memory");
+}
+
+template <int G>
+__global__ void __launch_bounds__(DD_THREADS, 1)
+    dedisp_f32_ring_kernel(const DedispLaunch p, const float* __restrict__ rows,
+                           float* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    constexpr int TPW = 2, TB = DD_WARPS * TPW, NS = FRING_NS, D = NS - 1;
+    extern __shared__ __align__(16) uint8_t smem[];
+    const uint32_t W = p.wmax;  // floats per channel window
+    float* buf = reinterpret_cast<float*>(smem);                                        // [NS][G][W]
+    uint32_t* offs = reinterpret_cast<uint32_t*>(smem + (size_t)NS * G * W * 4);       // [NS][G][TB]
+    uint64_t* full = reinterpret_cast<uint64_t*>(offs + NS * G * TB);                  // [NS]
+    uint64_t* empty = full + NS;                                                        // [NS]
+
+    const uint32_t blk = blockIdx.x;
+    const uint32_t row0 = blk * TB;
+    const uint32_t nrows_blk = min((uint32_t)TB, p.nrows - row0);
+    const uint64_t i0 = (uint64_t)blockIdx.y * DD_NT;
+    if (i0 >= blk_len[blk]) return;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t C = p.nchans;
+    const uint32_t nstages = (C + G - 1) / G;
+    constexpr int wpc = DD_WARPS / G;
+    const int my_cs = warp / wpc;
+    const uint32_t my_t = (uint32_t)((warp % wpc) * 32 + lane);
+    constexpr uint32_t vstride = (uint32_t)wpc * 32;
+    const uint32_t* offtab = p.dd_off + (size_t)blk * p.nchans_pad * TB;
+    const uint2* wintab = p.dd_win + (size_t)blk * p.nchans_pad;
+    const float* rows_i0 = rows + i0;
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            ring_init(full + s, DD_THREADS);
+            ring_init(empty + s, DD_WARPS);
+        }
+    }
+    __syncthreads();
+
+    auto issue = [&](uint32_t gi, int slot) {
+        const uint32_t c = gi * G + my_cs;
+        if (c < C) {
+            const uint2 wv = __ldg(wintab + c);
+            const float* src = rows_i0 + (size_t)c * p.rows_pitch + wv.x;
+            float* dst = buf + (size_t)(slot * G + my_cs) * W;
+            for (uint32_t vi = my_t; vi < wv.y; vi += vstride)
+                __pipeline_memcpy_async(dst + 4 * vi, src + 4 * vi, 16);
+        }
+        if ((int)threadIdx.x < G * TB / 4)
+            __pipeline_memcpy_async(offs + slot * G * TB + 4 * threadIdx.x,
+                                    offtab + (size_t)gi * G * TB + 4 * threadIdx.x, 16);
+        cp_async_arrive(full + slot);
+    };
+
+    float acc[TPW][DD_FOUT];
+#pragma unroll
+    for (int u = 0; u < TPW; ++u)
+#pragma unroll
+        for (int m = 0; m < DD_FOUT; ++m) acc[u][m] = 0.0f;  // the reference starts from +0.0f
+
+    for (int d = 0; d < D; ++d)
+        if ((uint32_t)d < nstages) issue(d, d);
+    int slot = 0;
+    uint32_t ph = 0;
+    for (uint32_t gi = 0; gi < nstages; ++gi) {
+        ring_wait(full + slot, ph);
+        const uint32_t c0 = gi * G;
+        const int nch = (int)min((uint32_t)G, C - c0);
+        const uint32_t* offb = offs + slot * G * TB + warp * TPW;
+        const float* bufb = buf + (size_t)slot * G * W + lane;
+        for (int cs = 0; cs < nch; ++cs) {
+#pragma unroll
+            for (int u = 0; u < TPW; ++u) {
+                const float* src = bufb + (size_t)cs * W + offb[cs * TB + u];
+#pragma unroll
+                for (int m = 0; m < DD_FOUT; ++m) acc[u][m] = __fadd_rn(acc[u][m], src[32 * m]);
+            }
+        }
+        __syncwarp();
+        if (lane == 0) ring_arrive(empty + slot);
+        if (gi + D < nstages) {
+            // the slot of stage gi+D last held stage gi-1 (gi >= 1): all warps must be done
+            const uint32_t nxt = gi + D;
+            const int s2 = (int)(nxt % NS);
+            if (gi >= 1) ring_wait(empty + s2, ((gi - 1) / NS) & 1);
+            issue(nxt, s2);
+        }
+        if (++slot == NS) {
+            slot = 0;
+            ph ^= 1;
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < TPW; ++u) {
+        const uint32_t r = warp * TPW + u;
+        if (r < nrows_blk) {
+            float* dst = out + (size_t)(row0 + r) * p.out_pitch + i0;
+#pragma unroll
+            for (int m = 0; m < DD_FOUT; ++m) dst[lane + 32 * m] = acc[u][m];
+        }
+    }
+}
+
 // Overlap reuse: chunk k's first keep[r] outputs of row r are chunk k-1's outputs
 // [shift, shift + keep[r]) (same absolute samples, same input bytes), moved in place.
 __global__ void series_shift_kernel(int32_t* __restrict__ series, uint64_t pitch, uint64_t shift,
@@ -1089,10 +1221,37 @@ void launch_dd_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStrea
     PGB_CUDA(cudaGetLastError());
 }
 
+size_t fring_smem_bytes(int g, uint32_t wmax) {
+    return (size_t)FRING_NS * g * wmax * 4 + (size_t)FRING_NS * g * 32 * 4 + 2 * FRING_NS * sizeof(uint64_t);
+}
+
+void launch_ddf_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st) {
+    const uint64_t warps = (uint64_t)((p.nrows + 31) / 32) * p.nchans_pad;
+    ddf_table_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(p, win, off);
+    PGB_CUDA(cudaGetLastError());
+}
+
 void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st) {
     const size_t smem = dedisp_smem_bytes(false, p.g, p.wmax);
     const int tb = DD_WARPS * p.tpw;
     dim3 grid((p.nrows + tb - 1) / tb, p.ntiles);
+    if (p.tpw == 2 && p.dd_off && !getenv("PGB_F32_RING0")) {  // the f32 ring (table built)
+        int g = 8;
+        while (g > 1 && fring_smem_bytes(g, p.wmax) > 227 * 1024) g >>= 1;
+        const size_t rsm = fring_smem_bytes(g, p.wmax);
+        if (rsm <= 227 * 1024) {
+#define PGB_FRING(G_)                                                                             \
+    if (g == G_) {                                                                                \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_f32_ring_kernel<G_>,                                 \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \
+        dedisp_f32_ring_kernel<G_><<<grid, DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len);       \
+        PGB_CUDA(cudaGetLastError());                                                             \
+        return;                                                                                   \
+    }
+            PGB_FRING(8) PGB_FRING(4) PGB_FRING(2) PGB_FRING(1)
+#undef PGB_FRING
+        }
+    }
     if (p.tpw == 2) {
         PGB_CUDA(cudaFuncSetAttribute(dedisp_f32_kernel<2>,
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

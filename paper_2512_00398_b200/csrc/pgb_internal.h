@@ -124,6 +124,9 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
 // builds p.dd_win / p.dd_off for the active set (tile independent; p.wmax = bytes per copy)
 void launch_dd_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st);
 void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cudaStream_t st);
+// f32 staging table (window start / float4 count per (block, channel), float offset per
+// trial) for the f32 ring kernel; p.wmax in floats
+void launch_ddf_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st);
 // series[r][i] = series[r][shift + i] for i < keep[r] (disjoint: shift >= keep[r])
 void launch_series_shift(int32_t* series, uint32_t nrows, uint64_t pitch, uint64_t shift,
                          const uint32_t* keep, cudaStream_t st);
