@@ -13,6 +13,7 @@
 #include <numeric>
 #include <stdexcept>
 
+#include <chrono>
 #include <cstdio>
 
 #include "pgb_internal.h"
@@ -150,6 +151,7 @@ struct pgb_context {
     // PGB_TRACE=1: an event after each stage of a file search, printed as a timeline
     bool trace = false;
     std::vector<std::pair<std::string, cudaEvent_t>> trace_ev;
+    std::vector<double> trace_host;  // host clock (ms) when each mark was issued
     DevBuf cl_scratch, clusters, members;
     PinnedBuf h_counters;
     RfiWork rfi;
@@ -273,8 +275,13 @@ void stage_h2d(pgb_context* ctx, void* dst, const void* src, size_t bytes, cudaS
     launch_copy_from_host(dst, p, bytes, st);
 }
 
+double host_ms() {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
 void trace_mark(pgb_context* ctx, const char* name, cudaStream_t s) {
     if (!ctx->trace) return;
+    ctx->trace_host.push_back(host_ms());
     cudaEvent_t e;
     PGB_CUDA(cudaEventCreate(&e));
     PGB_CUDA(cudaEventRecord(e, s));
@@ -285,12 +292,16 @@ void trace_dump(pgb_context* ctx) {
     if (!ctx->trace || ctx->trace_ev.empty()) return;
     PGB_CUDA(cudaDeviceSynchronize());
     float prev = 0.f;
+    size_t k = 0;
     for (auto& [name, e] : ctx->trace_ev) {
         float t = 0.f;
         PGB_CUDA(cudaEventElapsedTime(&t, ctx->trace_ev.front().second, e));
-        fprintf(stderr, "[pgb trace] %9.3f ms  +%8.3f  %s\n", t, t - prev, name.c_str());
+        const double hm = k < ctx->trace_host.size() ? ctx->trace_host[k] - ctx->trace_host.front() : 0.0;
+        fprintf(stderr, "[pgb trace] %9.3f ms  +%8.3f  (host %8.3f)  %s\n", t, t - prev, hm, name.c_str());
         prev = t;
+        ++k;
     }
+    ctx->trace_host.clear();
     for (auto& [name, e] : ctx->trace_ev) cudaEventDestroy(e);
     ctx->trace_ev.clear();
 }

@@ -165,6 +165,41 @@ __global__ void link_kernel(const pgb_candidate* __restrict__ c, uint64_t n, Cel
     }
 }
 
+// Default linking: one warp per candidate, the lanes split the members of each of the
+// 27 neighbour cells, the forest in global memory, CTAs across the whole GPU.  A bright
+// pulse puts hundreds to thousands of mutually linked candidates into a few cells; with
+// one thread per candidate walking them serially (below) a 1896-candidate config-A file
+// took 2.35 ms, a one-CTA shared-memory forest did not help (the walks, not the loads,
+// are serial).  Pairs are tested once (j > i); roots are compared before the box test.
+__global__ void __launch_bounds__(256)
+    link_warp_kernel(const pgb_candidate* __restrict__ c, uint64_t n, CellGeom g,
+                     const uint64_t* __restrict__ skeys, const uint32_t* __restrict__ sidx,
+                     uint32_t* parent) {
+    const uint64_t i = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t lane = threadIdx.x & 31;
+    if (i >= n) return;
+    const pgb_candidate a = c[i];
+    const int64_t kt = (int64_t)(a.peak_sample / g.cell_t());
+    const int64_t kd = (int64_t)(a.dm_trial / g.cell_dm());
+    const int64_t kw = (int64_t)(a.width_index / g.cell_w());
+    for (int64_t dt = -1; dt <= 1; ++dt) {
+        if (kt + dt < 0) continue;
+        for (int64_t dd = -1; dd <= 1; ++dd) {
+            if (kd + dd < 0) continue;
+            for (int64_t dw = -1; dw <= 1; ++dw) {
+                if (kw + dw < 0) continue;
+                const uint64_t key = cell_key(kt + dt, kd + dd, kw + dw);
+                const uint64_t p0 = lower_bound(skeys, n, key);
+                for (uint64_t p = p0 + lane; p < n && skeys[p] == key; p += 32) {
+                    const uint32_t j = sidx[p];
+                    if (j <= i || uf_find(parent, (uint32_t)i) == uf_find(parent, j)) continue;
+                    if (linked(a, c[j], g.r)) uf_unite(parent, (uint32_t)i, j);
+                }
+            }
+        }
+    }
+}
+
 // Small sets (n <= LINK_SMEM_MAX): the same linking with the union-find forest in
 // shared memory, one CTA.  The global version's finds are chains of uncached L2 loads
 // (~0.5 us each), which made a config-B link_grid (~600 candidates in a few dense
@@ -454,12 +489,16 @@ void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_r
     cub::DoubleBuffer<uint64_t> ck(keys_a, keys_b);
     cub::DoubleBuffer<uint32_t> cv(idx_a, idx_b);
     PGB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, sort_tmp, ck, cv, (int)n, 0, 64, st));
-    const int link_mode = [] {  // ablation: PGB_LINK_GLOBAL=1 / PGB_LINK_SMEM1=1
+    const int link_mode = [] {  // ablation: PGB_LINK_GLOBAL / PGB_LINK_SMEM1 / PGB_LINK_SMEM2
         if (getenv("PGB_LINK_GLOBAL")) return 2;
         if (getenv("PGB_LINK_SMEM1")) return 1;
+        if (getenv("PGB_LINK_SMEM2")) return 3;
         return 0;
     }();
-    if (n <= LINK_SMEM2_MAX && link_mode == 0) {
+    if (link_mode == 0) {
+        link_warp_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(cands, n, g, ck.Current(),
+                                                                            cv.Current(), parent);
+    } else if (n <= LINK_SMEM2_MAX && link_mode == 3) {
         const size_t smem = (size_t)40 * n;
         PGB_CUDA(cudaFuncSetAttribute(link_smem2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                       (int)(40 * LINK_SMEM2_MAX)));

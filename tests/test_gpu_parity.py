@@ -247,17 +247,18 @@ def test_link_grid_vs_reference_library(engine, ref):
 @pytest.mark.parametrize("n,extent", [(3000, 20_000), (5120, 200_000), (12288, 2_000_000),
                                       (20000, 3_000_000)])
 def test_link_grid_smem_and_global_forests_agree(engine, port, monkeypatch, n, extent):
-    """link_grid links sets of <= 5120 candidates with everything staged in shared memory,
-    <= 12288 with a shared-memory forest and larger ones with the global one; every variant
-    must give the reference clusters (dense sets make big components and contended unions)."""
+    """link_grid's linking variants -- warp per candidate over a global forest (default),
+    one CTA with everything staged in shared memory (<= 5120), one CTA with a shared-memory
+    forest (<= 12288), thread per candidate over a global forest -- must all give the
+    reference clusters (dense sets make big components and contended unions)."""
     rng = np.random.default_rng(n)
     cands = random_candidates(rng, n, extent)
     recs, members = port.link_grid(cands, (3, 9, 3))
-    clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)
-    monkeypatch.setenv("PGB_LINK_SMEM1", "1")
-    clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)
-    monkeypatch.setenv("PGB_LINK_GLOBAL", "1")
-    clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)
+    clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)  # warp per candidate
+    for mode in ("PGB_LINK_SMEM2", "PGB_LINK_SMEM1", "PGB_LINK_GLOBAL"):
+        monkeypatch.setenv(mode, "1")
+        clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)
+        monkeypatch.delenv(mode)
 
 
 def test_link_grid_ties(engine):
