@@ -56,6 +56,22 @@ def test_dedisperse_f32_bit_exact(engine, port, nchans, L):
         assert np.array_equal(got[t], port.dedisperse(data, plan.delays[t])), t
 
 
+@pytest.mark.parametrize("nchans,foff,L,dm_hi,step", [
+    (2048, -0.14, 24000, 800.0, 8.0),     # wide windows: fewer channels per ring stage
+    (1000, -0.3, 20000, 1500.0, 33.0),    # 46 trials: a partial second block, nchans % 8 != 0
+])
+def test_dedisperse_f32_ring_wide_windows(engine, port, nchans, foff, L, dm_hi, step):
+    """fp32 ring kernel (non-integer data): in-order fp32 sums bit-exact for sampled trials
+    of plans whose per-block delay spreads force narrow stages."""
+    hdr = FilterbankHeader(fch1=1500.0, foff=foff, nchans=nchans, tsamp=64e-6)
+    plan = generate_dm_trials(0.0, dm_hi, hdr, LinearSpacing(step))
+    data = f32_chunk(nchans, L, seed=nchans + 1, scale=5.0)
+    ok = [t for t in range(plan.ntrials) if plan.trial_max_delay(t) < L]
+    got = engine.dedisperse(data, plan, range(0, len(ok)))
+    for t in ok[::max(1, len(ok) // 8)] + [ok[-1]]:
+        assert np.array_equal(got[t], port.dedisperse(data, plan.delays[t])), t
+
+
 def test_dedisperse_chunk_too_short(engine):
     # tests/test_dedisp.cpp:245-257
     hdr = FilterbankHeader(fch1=1500.0, foff=-50.0, nchans=8, tsamp=64e-6)
