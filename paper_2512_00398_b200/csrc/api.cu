@@ -129,7 +129,7 @@ struct pgb_context {
     // (transpose, dedispersion, baseline, RMS) to its back half (boxcar, runs, order)
     DevBuf base[2], frms[2], status[2], d_row_len[2], slot_active[2];
     DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
-    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off, d_keep, d_work;
+    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off, d_keep, d_work, d_bsums;
     // what the series buffer holds: the dedispersed rows of the raw-sample chunk
     // [ser_start, ser_start + ser_len) at pitch ser_pitch (overlap reuse)
     bool ser_ok = false;
@@ -613,8 +613,15 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     if (baseline) {
         const uint64_t w = cfg->baseline_window % 2 == 0 ? cfg->baseline_window + 1 : cfg->baseline_window;
         if (u8)
+        {
+            long long* bsums = nullptr;
+            if (!getenv("PGB_BASELINE_SERIAL")) {
+                ctx->d_bsums.reserve(baseline_block_sums_bytes(nrows, out_pitch));
+                bsums = ctx->d_bsums.as<long long>();
+            }
             launch_baseline_int(ctx->series.as<int32_t>(), ctx->base[slot].as<float>(), d_len, nrows,
-                                out_pitch, w, st);
+                                out_pitch, w, bsums, st);
+        }
         else
             launch_baseline_f32(ctx->series.as<float>(), ctx->base[slot].as<float>(), d_len, nrows,
                                 out_pitch, w, st);
@@ -959,6 +966,7 @@ pgb_status pgb_destroy(pgb_context* ctx) {
                               &ctx->slot_active[k]})
                 b->release();
         ctx->d_work.release();
+        ctx->d_bsums.release();
         ctx->d_keep.release();
         ctx->file_ctr.release();
         for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,

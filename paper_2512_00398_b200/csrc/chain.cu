@@ -127,6 +127,153 @@ __global__ void __launch_bounds__(BL_THREADS)
     }
 }
 
+// ---- baseline, warp segments (default) -------------------------------------------
+// The row-serial kernel above walks each row's ~60 tiles in order (3 CTA barriers and a
+// global-load round trip per tile) and is latency-bound at ~18 % of HBM bandwidth.  Here
+// every warp owns a 4096-sample segment of a row: its starting window sum comes from
+// 256-sample block sums (<= 2 x 255 edge samples + <= 123 block sums), then it scans its
+// segment 128 samples at a time with warp shuffles only.  All sums are exact int64, so
+// the output is the same bit for bit.
+constexpr int BW_BLK = 256;   // block-sum granule (samples)
+constexpr int BW_SEG = 4096;  // samples per warp segment
+
+__device__ __forceinline__ long long warp_sum_ll(long long v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(256)
+    block256_sums_kernel(const int32_t* __restrict__ x_all, const uint32_t* __restrict__ row_len,
+                         uint64_t pitch, uint32_t nrows, uint32_t nb, long long* __restrict__ bs) {
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= (uint64_t)nrows * nb) return;
+    const uint32_t row = (uint32_t)(gw / nb), b = (uint32_t)(gw % nb);
+    const int64_t n = row_len[row];
+    const int64_t lo = (int64_t)b * BW_BLK;
+    long long s = 0;
+    if (lo < n) {
+        const int32_t* x = x_all + (size_t)row * pitch;
+        const int64_t hi = lo + BW_BLK < n ? lo + BW_BLK : n;
+        for (int64_t i = lo + lane; i < hi; i += 32) s += x[i];
+    }
+    s = warp_sum_ll(s);
+    if (lane == 0) bs[(size_t)row * nb + b] = s;
+}
+
+__global__ void __launch_bounds__(256)
+    baseline_warp_kernel(const int32_t* __restrict__ x_all, float* __restrict__ out_all,
+                         const uint32_t* __restrict__ row_len, uint64_t pitch, uint64_t window,
+                         uint32_t nrows, uint32_t nseg, uint32_t nb, const long long* __restrict__ bsum) {
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= (uint64_t)nrows * nseg) return;
+    const uint32_t row = (uint32_t)(gw / nseg), seg = (uint32_t)(gw % nseg);
+    const int64_t n = row_len[row];
+    const int64_t s0 = (int64_t)seg * BW_SEG;
+    if (s0 >= n) return;
+    const int64_t s1 = s0 + BW_SEG < n ? s0 + BW_SEG : n;
+    const int32_t* x = x_all + (size_t)row * pitch;
+    float* out = out_all + (size_t)row * pitch;
+    const long long* bs = bsum + (size_t)row * nb;
+    const int64_t h = (int64_t)(window / 2);
+    if (h >= n - 1) {  // global-mean path, src/detect.cpp:16-32 (row total from its blocks)
+        long long t = 0;
+        for (int64_t b = lane; b * BW_BLK < n; b += 32) t += bs[b];
+        const long long total = warp_sum_ll(t);
+        const float mean = __double2float_rn(__ddiv_rn((double)total, (double)n));
+        for (int64_t i = s0 + lane; i < s1; i += 32) out[i] = __fsub_rn((float)x[i], mean);
+        return;
+    }
+    const double inv_full = __ddiv_rn(1.0, (double)(2 * h + 1));
+    // window sum at s0 over [lo, hi]: whole 256-sample blocks plus the two partial ends
+    const int64_t lo = s0 - h > 0 ? s0 - h : 0, hi = s0 + h < n - 1 ? s0 + h : n - 1;
+    const int64_t blo = (lo + BW_BLK - 1) / BW_BLK, bhi = (hi + 1) / BW_BLK - 1;
+    long long part = 0;
+    if (blo <= bhi) {
+        for (int64_t b = blo + lane; b <= bhi; b += 32) part += bs[b];
+        for (int64_t i = lo + lane; i < blo * BW_BLK; i += 32) part += x[i];
+        for (int64_t i = (bhi + 1) * BW_BLK + lane; i <= hi; i += 32) part += x[i];
+    } else {
+        for (int64_t i = lo + lane; i <= hi; i += 32) part += x[i];
+    }
+    long long carry = warp_sum_ll(part);  // S_{s0}; d_{s0} := 0 below
+    if (s0 >= h + 1 && s1 - 1 + h <= n - 1) {
+        // interior segment: every window is whole (one reciprocal), every x[i +- h] exists;
+        // 32-bit indices and differences (|d| < 2^21, 128-sample prefix < 2^28), the
+        // window sum itself stays int64
+        const uint32_t hh = (uint32_t)h;
+        for (uint32_t base = (uint32_t)s0; base < (uint32_t)s1; base += 128) {
+            const uint32_t i4 = base + 4 * lane;
+            const int4 xq = *reinterpret_cast<const int4*>(x + i4);  // 16-byte aligned (pitch, base)
+            const int32_t xv[4] = {xq.x, xq.y, xq.z, xq.w};
+            int32_t d[4];
+            int32_t local = 0;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const uint32_t i = i4 + k;
+                d[k] = (i > (uint32_t)s0 && i < (uint32_t)s1) ? x[i + hh] - x[i - 1 - hh] : 0;
+                local += d[k];
+            }
+            int32_t incl = local;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= o) incl += y;
+            }
+            long long run = carry + (long long)(incl - local);
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                run += d[k];
+                if (i4 + k < (uint32_t)s1)
+                    out[i4 + k] = __double2float_rn(__fma_rn(-(double)run, inv_full, (double)xv[k]));  // :45
+            }
+            carry += __shfl_sync(0xffffffffu, incl, 31);
+        }
+        return;
+    }
+    for (int64_t base = s0; base < s1; base += 128) {
+        long long d[4];
+        int32_t xv[4];
+        long long local = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = base + 4 * lane + k;
+            long long di = 0;
+            int32_t xi = 0;
+            if (i < s1) {
+                xi = x[i];
+                if (i > s0) {
+                    if (i + h < n) di += x[i + h];
+                    if (i - 1 - h >= 0) di -= x[i - 1 - h];
+                }
+            }
+            d[k] = di;
+            xv[k] = xi;
+            local += di;
+        }
+        long long incl = local;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        long long run = carry + (incl - local);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = base + 4 * lane + k;
+            run += d[k];
+            if (i < s1) {
+                const int64_t wlo = i - h > 0 ? i - h : 0;
+                const int64_t whi = i + h < n - 1 ? i + h : n - 1;
+                const int64_t cnt = whi - wlo + 1;
+                // interior windows share one reciprocal; only the 2h edge samples divide
+                const double inv = cnt == 2 * h + 1 ? inv_full : __ddiv_rn(1.0, (double)cnt);
+                out[i] = __double2float_rn(__fma_rn(-(double)run, inv, (double)xv[k]));  // :45
+            }
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
 // ---- baseline: general float series (sequential replay, one thread per trial) ---
 
 __global__ void baseline_f32_kernel(const float* __restrict__ x_all, float* __restrict__ out_all,
@@ -570,10 +717,24 @@ __global__ void stitch_kernel(const Fragment* __restrict__ f, uint64_t nf,
 }  // namespace
 
 void launch_baseline_int(const int32_t* x, float* out, const uint32_t* row_len, uint32_t nrows,
-                         uint64_t pitch, uint64_t window, cudaStream_t st) {
+                         uint64_t pitch, uint64_t window, long long* block_sums, cudaStream_t st) {
     if (!nrows) return;
-    baseline_int_kernel<<<nrows, BL_THREADS, 0, st>>>(x, out, row_len, pitch, window);
+    if (!block_sums) {  // row-serial kernel (ablation: PGB_BASELINE_SERIAL=1)
+        baseline_int_kernel<<<nrows, BL_THREADS, 0, st>>>(x, out, row_len, pitch, window);
+    } else {
+        const uint32_t nb = (uint32_t)((pitch + BW_BLK - 1) / BW_BLK);
+        const uint32_t nseg = (uint32_t)((pitch + BW_SEG - 1) / BW_SEG);  // pitch >= every row length
+        const uint64_t w1 = (uint64_t)nrows * nb, w2 = (uint64_t)nrows * nseg;
+        block256_sums_kernel<<<(unsigned)((w1 * 32 + 255) / 256), 256, 0, st>>>(x, row_len, pitch, nrows, nb,
+                                                                                 block_sums);
+        baseline_warp_kernel<<<(unsigned)((w2 * 32 + 255) / 256), 256, 0, st>>>(x, out, row_len, pitch, window,
+                                                                                nrows, nseg, nb, block_sums);
+    }
     PGB_CUDA(cudaGetLastError());
+}
+
+size_t baseline_block_sums_bytes(uint32_t nrows, uint64_t pitch) {
+    return (size_t)nrows * ((pitch + BW_BLK - 1) / BW_BLK) * sizeof(long long);
 }
 
 void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, uint32_t nrows,

@@ -139,8 +139,11 @@ void launch_ws_offsets(const DedispLaunch& p, uint32_t* wbase, uint16_t* woff, c
 bool dedisp_ws_available();
 
 // chain
+// block_sums: scratch of baseline_block_sums_bytes (warp-segment kernels, default), or
+// null for the row-serial kernel
 void launch_baseline_int(const int32_t* x, float* out, const uint32_t* row_len, uint32_t nrows,
-                         uint64_t pitch, uint64_t window, cudaStream_t st);
+                         uint64_t pitch, uint64_t window, long long* block_sums, cudaStream_t st);
+size_t baseline_block_sums_bytes(uint32_t nrows, uint64_t pitch);
 void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, uint32_t nrows,
                          uint64_t pitch, uint64_t window, cudaStream_t st);
 // input kind: 0 = float baseline output, 1 = int32 series, 2 = float series
