@@ -1,0 +1,52 @@
+"""Every dedispersion kernel variant the launcher can pick is bit-exact: the env switches
+are read once per process, so each variant runs in its own interpreter on a few of the
+parity shapes (dedispersed sums against the C restatement of the naive definition)."""
+import os
+import subprocess
+import sys
+from pathlib import Path
+
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+ROOT = Path(__file__).resolve().parents[1]
+
+SNIPPET = r'''
+import sys
+sys.path.insert(0, {root!r})
+import numpy as np
+from oracle.pyoracle import Port
+from paper_2512_00398_b200.dedisp import FilterbankHeader, LinearSpacing, generate_dm_trials
+from paper_2512_00398_b200.engine import Engine
+from tests.helpers import u8_chunk, f32_chunk
+port = Port()
+cases = [(4096, 1518.0, -0.0703125, 24000, 800.0, 8.0), (1024, 1500.0, -0.25, 20000, 500.0, 2.0),
+         (517, 1450.0, -0.5, 12000, 400.0, 2.5)]
+with Engine(0) as eng:
+    for nch, fch1, foff, L, dm_hi, step in cases:
+        hdr = FilterbankHeader(fch1=fch1, foff=foff, nchans=nch, tsamp=64e-6)
+        plan = generate_dm_trials(0.0, dm_hi, hdr, LinearSpacing(step))
+        for data in (u8_chunk(hdr, plan, L, seed=nch), f32_chunk(nch, L, seed=nch, scale=5.0)):
+            ok = [t for t in range(plan.ntrials) if plan.trial_max_delay(t) < L]
+            got = eng.dedisperse(data, plan, range(0, len(ok)))
+            for t in ok[::max(1, len(ok) // 6)] + [ok[-1]]:
+                want = port.dedisperse(data.astype(np.float32) if data.dtype == np.uint8 else data,
+                                       plan.delays[t])
+                assert np.array_equal(got[t], want), (nch, t)
+print("ok")
+'''
+
+
+@pytest.mark.parametrize("env", [
+    {},                                   # persistent ring (u8), fp32 ring
+    {"PGB_DD_PERSIST0": "1"},             # grid-launched ring
+    {"PGB_DD_RING": "0"},                 # CTA-barrier table kernel
+    {"PGB_RING_MODE": "2"},               # ring with IMAD addressing
+    {"PGB_F32_RING0": "1"},               # fp32 two-barrier kernel
+])
+def test_dedispersion_variants_bit_exact(env):
+    e = dict(os.environ, **env)
+    out = subprocess.run([sys.executable, "-c", SNIPPET.format(root=str(ROOT))], env=e,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
