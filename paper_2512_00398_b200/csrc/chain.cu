@@ -556,11 +556,11 @@ __global__ void __launch_bounds__(BX_THREADS)
     constexpr bool kPad = S == 16;
     constexpr uint32_t LD = kPad ? N + N / 4 : N;
     extern __shared__ double sbuf[];  // ping-pong [2][LD]
-    const uint32_t row = blockIdx.y;
+    const uint32_t row = blockIdx.x;  // rows on x: more than 65535 trials are legal
     if (status[row]) return;
     const uint64_t n = row_len[row];
     const uint32_t T = N - (uint32_t)bmax;
-    const uint64_t i0 = (uint64_t)blockIdx.x * T;
+    const uint64_t i0 = (uint64_t)blockIdx.y * T;
     if (i0 >= n) return;
     const float frms = frms_all[row];
     const int tid = threadIdx.x;
@@ -788,7 +788,7 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
     const uint64_t T = N - bmax;
     const unsigned tiles = (unsigned)((max_len + T - 1) / T);
     const size_t smem = 2 * LD * sizeof(double);
-    dim3 grid(tiles, nrows);
+    dim3 grid(nrows, tiles);
 #define PGB_BX(K, SS)                                                                        \
     do {                                                                                     \
         PGB_CUDA(cudaFuncSetAttribute(boxcar_peaks_kernel<K, SS>,                            \

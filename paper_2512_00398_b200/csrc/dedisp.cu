@@ -972,9 +972,9 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 // [shift, shift + keep[r]) (same absolute samples, same input bytes), moved in place.
 __global__ void series_shift_kernel(int32_t* __restrict__ series, uint64_t pitch, uint64_t shift,
                                     const uint32_t* __restrict__ keep) {
-    int32_t* row = series + (size_t)blockIdx.y * pitch;
-    const uint32_t n = keep[blockIdx.y];
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    int32_t* row = series + (size_t)blockIdx.x * pitch;  // rows on x (any trial count)
+    const uint32_t n = keep[blockIdx.x];
+    for (uint32_t i = blockIdx.y * blockDim.x + threadIdx.x; i < n; i += gridDim.y * blockDim.x)
         row[i] = row[shift + i];
 }
 
@@ -1267,7 +1267,7 @@ void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cud
 void launch_series_shift(int32_t* series, uint32_t nrows, uint64_t pitch, uint64_t shift,
                          const uint32_t* keep, cudaStream_t st) {
     if (!nrows) return;
-    series_shift_kernel<<<dim3(8, nrows), 512, 0, st>>>(series, pitch, shift, keep);
+    series_shift_kernel<<<dim3(nrows, 8), 512, 0, st>>>(series, pitch, shift, keep);
     PGB_CUDA(cudaGetLastError());
 }
 

@@ -102,3 +102,22 @@ def test_link_grid_partition_is_permutation_invariant(engine):
         return sorted(tuple(sorted(int(ids[m]) for m in cl.member_ids(i))) for i in range(len(cl)))
 
     assert partition(a, np.arange(len(cands))) == partition(b, perm)
+
+
+def test_more_than_65535_trials(engine, port):
+    """Trial rows index CUDA grid x dimensions (not y, capped at 65535): a 70001-trial
+    plan runs and matches the C restatement."""
+    from .helpers import cfg_dict
+
+    hdr = FilterbankHeader(fch1=1500.0, foff=-8.0, nchans=8, tsamp=64e-6)
+    plan = generate_dm_trials(0.0, 70.0, hdr, LinearSpacing(0.001))
+    assert plan.ntrials > 65535
+    L = 3000
+    data = u8_chunk(hdr, plan, L, seed=4, pulses=[(30000, 1200, 4, 40.0)])
+    cfg = EngineConfig(n_workers=1, tsamp=hdr.tsamp, boxcar_max=64, baseline_window=501)
+    spec = ChunkSpec.whole(L)
+    res = engine.run_dm_loop(Chunk(spec, data), plan, cfg)
+    want, want_sk = port.run_dm_loop(data, vars(spec), plan.dms, plan.delays, cfg_dict(cfg))
+    assert len(want) > 0
+    assert_same_candidates(res.candidates, want)
+    assert np.array_equal(res.skipped_trials, want_sk)
