@@ -129,7 +129,7 @@ struct pgb_context {
     // (transpose, dedispersion, baseline, RMS) to its back half (boxcar, runs, order)
     DevBuf base[2], frms[2], status[2], d_row_len[2], slot_active[2];
     DevBuf cands_raw, cands_sorted, frags, frags_sorted, counters, sort_keys, sort_idx, sort_tmp;
-    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off, d_keep, d_work, d_bsums;
+    DevBuf payload, in_u8, ws_base, ws_off, dd_win, dd_off, d_keep, d_work, d_bsums, d_lmin;
     // what the series buffer holds: the dedispersed rows of the raw-sample chunk
     // [ser_start, ser_start + ser_len) at pitch ser_pitch (overlap reuse)
     bool ser_ok = false;
@@ -623,8 +623,18 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                                 out_pitch, w, bsums, st);
         }
         else
+        {
+            long long* bsums = nullptr;
+            int* lmin = nullptr;
+            if (!getenv("PGB_BASELINE_SERIAL")) {
+                ctx->d_bsums.reserve(baseline_block_sums_bytes(nrows, out_pitch));
+                ctx->d_lmin.reserve(nrows * sizeof(int));
+                bsums = ctx->d_bsums.as<long long>();
+                lmin = ctx->d_lmin.as<int>();
+            }
             launch_baseline_f32(ctx->series.as<float>(), ctx->base[slot].as<float>(), d_len, nrows,
-                                out_pitch, w, st);
+                                out_pitch, w, bsums, lmin, st);
+        }
         work = ctx->base[slot].p;
         kind = 0;
     }
@@ -833,6 +843,7 @@ ChunkInput prepare_f32(pgb_context* ctx, const float* dptr, uint64_t length) {
     PGB_CUDA(cudaMemcpyAsync(hflag, dflag, sizeof *hflag, cudaMemcpyDeviceToHost, ctx->st));
     PGB_CUDA(cudaStreamSynchronize(ctx->st));
     ctx->launches += 1;
+    trace_mark(ctx, "integer check (pack)", ctx->st);
     if (*hflag == 0) return ChunkInput{ctx->in_u8.p, true};
     return ChunkInput{dptr, false};
 }
@@ -967,6 +978,7 @@ pgb_status pgb_destroy(pgb_context* ctx) {
                 b->release();
         ctx->d_work.release();
         ctx->d_bsums.release();
+        ctx->d_lmin.release();
         ctx->d_keep.release();
         ctx->file_ctr.release();
         for (DevBuf* b : {&ctx->d_delays_ct, &ctx->d_dms, &ctx->in_raw, &ctx->rows, &ctx->series,
@@ -1411,6 +1423,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                     rfi_clean_impl<uint8_t>(cptr, chunks[k].length, C, to_rfi(rfi), ctx->rfi, ctx->rfi_out.as<float>(),
                                             ctx->st, &nbc, &nbs);
                     ctx->launches += 8;
+                    trace_mark(ctx, "rfi excision", ctx->st);
                     if (nbc || nbs) {
                         ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
                         ci.pitch_min = pitch_min;

@@ -274,13 +274,191 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// ---- baseline, float series: exact fixed point when provably exact -----------------
+// The reference's running double window sum (src/detect.cpp:34-54) is order dependent in
+// general, so a float series is replayed sequentially per trial (below).  But if every
+// value is a multiple of 2^L and (2h+2) max|x| < 2^(53+L), every partial sum the reference
+// forms is exactly representable, so its running sum equals the exact window sum -- which
+// int64 fixed point (x * 2^-L) computes in any order.  f32_row_range_kernel measures L and
+// the largest exponent per row; rows that pass run the parallel warp-segment algorithm,
+// the rest (if any) the sequential replay.  Config E's masked float chunks all pass
+// (sequential replay: 167 ms per 2^19-sample chunk, one uncoalesced thread per trial).
+constexpr int FR_NOT_EXACT = -100000;
+
+__global__ void __launch_bounds__(256)
+    f32_row_range_kernel(const float* __restrict__ x_all, const uint32_t* __restrict__ row_len,
+                         uint64_t pitch, uint64_t window, int* __restrict__ lmin_out) {
+    __shared__ int s_lo[8], s_hi[8], s_bad[8];
+    const uint32_t row = blockIdx.x;
+    const int64_t n = row_len[row];
+    const float* x = x_all + (size_t)row * pitch;
+    int lo = 1 << 20, hi = -(1 << 20), bad = 0;
+    for (int64_t i = threadIdx.x; i < n; i += blockDim.x) {
+        const uint32_t mag = __float_as_uint(x[i]) & 0x7fffffffu;
+        if (mag == 0) continue;
+        if (mag >= 0x7f800000u) { bad = 1; continue; }
+        const int e = (int)(mag >> 23);
+        const uint32_t m = e ? ((mag & 0x7fffffu) | 0x800000u) : (mag & 0x7fffffu);
+        const int E = e ? e - 127 : -126;
+        lo = min(lo, E - 23 + (__ffs((int)m) - 1));  // exponent of the lowest set bit
+        hi = max(hi, E);                              // |x| < 2^(E+1)
+    }
+    for (int o = 16; o; o >>= 1) {
+        lo = min(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+        hi = max(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        bad |= __shfl_xor_sync(0xffffffffu, bad, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+        s_bad[threadIdx.x >> 5] = bad;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) {
+            lo = min(lo, s_lo[w]);
+            hi = max(hi, s_hi[w]);
+            bad |= s_bad[w];
+        }
+        int res;
+        if (bad) {
+            res = FR_NOT_EXACT;
+        } else if (hi < lo) {  // all zero: L = 0 works
+            res = 0;
+        } else {
+            // any partial sum is a sum of <= 2h+2 values of magnitude < 2^(hi+1)
+            const uint64_t terms = 2 * (window / 2) + 2;
+            int lg = 0;
+            while ((1ull << lg) < terms) ++lg;
+            res = (hi + 1 + lg <= 52 + lo) ? lo : FR_NOT_EXACT;
+        }
+        lmin_out[row] = res;
+    }
+}
+
+__device__ __forceinline__ double pow2d(int k) {  // 2^k for |k| < 1000, exact
+    return __longlong_as_double((long long)(1023 + k) << 52);
+}
+
+__device__ __forceinline__ long long f32_fixed(float v, double sc) {  // v * 2^-L, exact by the row check
+    return __double2ll_rn(__dmul_rn((double)v, sc));
+}
+
+__global__ void __launch_bounds__(256)
+    block256_sums_f32_kernel(const float* __restrict__ x_all, const uint32_t* __restrict__ row_len,
+                             uint64_t pitch, uint32_t nrows, uint32_t nb, const int* __restrict__ lmin,
+                             long long* __restrict__ bs) {
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= (uint64_t)nrows * nb) return;
+    const uint32_t row = (uint32_t)(gw / nb), b = (uint32_t)(gw % nb);
+    const int L = lmin[row];
+    if (L == FR_NOT_EXACT) return;
+    const double sc = pow2d(-L);
+    const int64_t n = row_len[row];
+    const int64_t lo = (int64_t)b * BW_BLK;
+    long long s = 0;
+    if (lo < n) {
+        const float* x = x_all + (size_t)row * pitch;
+        const int64_t hi = lo + BW_BLK < n ? lo + BW_BLK : n;
+        for (int64_t i = lo + lane; i < hi; i += 32) s += f32_fixed(x[i], sc);
+    }
+    s = warp_sum_ll(s);
+    if (lane == 0) bs[(size_t)row * nb + b] = s;
+}
+
+__global__ void __launch_bounds__(256)
+    baseline_warp_f32_kernel(const float* __restrict__ x_all, float* __restrict__ out_all,
+                             const uint32_t* __restrict__ row_len, uint64_t pitch, uint64_t window,
+                             uint32_t nrows, uint32_t nseg, uint32_t nb, const long long* __restrict__ bsum,
+                             const int* __restrict__ lmin) {
+    const uint64_t gw = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= (uint64_t)nrows * nseg) return;
+    const uint32_t row = (uint32_t)(gw / nseg), seg = (uint32_t)(gw % nseg);
+    const int L = lmin[row];
+    if (L == FR_NOT_EXACT) return;  // replayed sequentially by baseline_f32_kernel
+    const double sc = pow2d(-L), usc = pow2d(L);
+    const int64_t n = row_len[row];
+    const int64_t s0 = (int64_t)seg * BW_SEG;
+    if (s0 >= n) return;
+    const int64_t s1 = s0 + BW_SEG < n ? s0 + BW_SEG : n;
+    const float* x = x_all + (size_t)row * pitch;
+    float* out = out_all + (size_t)row * pitch;
+    const long long* bs = bsum + (size_t)row * nb;
+    const int64_t h = (int64_t)(window / 2);
+    if (h >= n - 1) {  // global-mean path: the 4-chain double sum is exact here too
+        long long t = 0;
+        for (int64_t b = lane; b * BW_BLK < n; b += 32) t += bs[b];
+        const long long total = warp_sum_ll(t);
+        const double tot = __dmul_rn((double)total, usc);
+        const float mean = __double2float_rn(__ddiv_rn(tot, (double)n));
+        for (int64_t i = s0 + lane; i < s1; i += 32) out[i] = __fsub_rn(x[i], mean);
+        return;
+    }
+    const double inv_full = __ddiv_rn(1.0, (double)(2 * h + 1));
+    const int64_t lo = s0 - h > 0 ? s0 - h : 0, hi = s0 + h < n - 1 ? s0 + h : n - 1;
+    const int64_t blo = (lo + BW_BLK - 1) / BW_BLK, bhi = (hi + 1) / BW_BLK - 1;
+    long long part = 0;
+    if (blo <= bhi) {
+        for (int64_t b = blo + lane; b <= bhi; b += 32) part += bs[b];
+        for (int64_t i = lo + lane; i < blo * BW_BLK; i += 32) part += f32_fixed(x[i], sc);
+        for (int64_t i = (bhi + 1) * BW_BLK + lane; i <= hi; i += 32) part += f32_fixed(x[i], sc);
+    } else {
+        for (int64_t i = lo + lane; i <= hi; i += 32) part += f32_fixed(x[i], sc);
+    }
+    long long carry = warp_sum_ll(part);  // S_{s0} in units of 2^L
+    for (int64_t base = s0; base < s1; base += 128) {
+        long long d[4];
+        float xv[4];
+        long long local = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = base + 4 * lane + k;
+            long long di = 0;
+            float xi = 0.0f;
+            if (i < s1) {
+                xi = x[i];
+                if (i > s0) {
+                    if (i + h < n) di += f32_fixed(x[i + h], sc);
+                    if (i - 1 - h >= 0) di -= f32_fixed(x[i - 1 - h], sc);
+                }
+            }
+            d[k] = di;
+            xv[k] = xi;
+            local += di;
+        }
+        long long incl = local;
+        for (int o = 1; o < 32; o <<= 1) {
+            const long long y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        long long run = carry + (incl - local);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int64_t i = base + 4 * lane + k;
+            run += d[k];
+            if (i < s1) {
+                const int64_t wlo = i - h > 0 ? i - h : 0;
+                const int64_t whi = i + h < n - 1 ? i + h : n - 1;
+                const int64_t cnt = whi - wlo + 1;
+                const double inv = cnt == 2 * h + 1 ? inv_full : __ddiv_rn(1.0, (double)cnt);
+                const double sum = __dmul_rn((double)run, usc);  // exact: |run| < 2^53
+                out[i] = __double2float_rn(__fma_rn(-sum, inv, (double)xv[k]));  // :45
+            }
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
 // ---- baseline: general float series (sequential replay, one thread per trial) ---
 
 __global__ void baseline_f32_kernel(const float* __restrict__ x_all, float* __restrict__ out_all,
                                     const uint32_t* __restrict__ row_len, uint32_t nrows,
-                                    uint64_t pitch, uint64_t window) {
+                                    uint64_t pitch, uint64_t window, const int* __restrict__ lmin) {
     const uint32_t row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= nrows) return;
+    if (lmin && lmin[row] != FR_NOT_EXACT) return;  // done by the fixed-point kernels
     const uint64_t n = row_len[row];
     const float* x = x_all + (size_t)row * pitch;
     float* out = out_all + (size_t)row * pitch;
@@ -738,9 +916,21 @@ size_t baseline_block_sums_bytes(uint32_t nrows, uint64_t pitch) {
 }
 
 void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, uint32_t nrows,
-                         uint64_t pitch, uint64_t window, cudaStream_t st) {
+                         uint64_t pitch, uint64_t window, long long* block_sums, int* row_lmin,
+                         cudaStream_t st) {
     if (!nrows) return;
-    baseline_f32_kernel<<<(nrows + 63) / 64, 64, 0, st>>>(x, out, row_len, nrows, pitch, window);
+    if (block_sums && row_lmin) {  // exact rows in fixed point, the rest replayed below
+        const uint32_t nb = (uint32_t)((pitch + BW_BLK - 1) / BW_BLK);
+        const uint32_t nseg = (uint32_t)((pitch + BW_SEG - 1) / BW_SEG);
+        const uint64_t w1 = (uint64_t)nrows * nb, w2 = (uint64_t)nrows * nseg;
+        f32_row_range_kernel<<<nrows, 256, 0, st>>>(x, row_len, pitch, window, row_lmin);
+        block256_sums_f32_kernel<<<(unsigned)((w1 * 32 + 255) / 256), 256, 0, st>>>(x, row_len, pitch, nrows, nb,
+                                                                                     row_lmin, block_sums);
+        baseline_warp_f32_kernel<<<(unsigned)((w2 * 32 + 255) / 256), 256, 0, st>>>(
+            x, out, row_len, pitch, window, nrows, nseg, nb, block_sums, row_lmin);
+    }
+    baseline_f32_kernel<<<(nrows + 63) / 64, 64, 0, st>>>(x, out, row_len, nrows, pitch, window,
+                                                          block_sums && row_lmin ? row_lmin : nullptr);
     PGB_CUDA(cudaGetLastError());
 }
 

@@ -144,8 +144,11 @@ bool dedisp_ws_available();
 void launch_baseline_int(const int32_t* x, float* out, const uint32_t* row_len, uint32_t nrows,
                          uint64_t pitch, uint64_t window, long long* block_sums, cudaStream_t st);
 size_t baseline_block_sums_bytes(uint32_t nrows, uint64_t pitch);
+// block_sums (baseline_block_sums_bytes) + row_lmin ([nrows] int): rows whose window sums
+// are provably exact in double run in int64 fixed point; null: sequential replay only
 void launch_baseline_f32(const float* x, float* out, const uint32_t* row_len, uint32_t nrows,
-                         uint64_t pitch, uint64_t window, cudaStream_t st);
+                         uint64_t pitch, uint64_t window, long long* block_sums, int* row_lmin,
+                         cudaStream_t st);
 // input kind: 0 = float baseline output, 1 = int32 series, 2 = float series
 // packed: 16 warps per block (runs beside other kernels), else one warp per block
 void launch_rms(const void* x, int kind, const uint32_t* row_len, uint32_t nrows, uint64_t pitch,

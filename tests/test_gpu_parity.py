@@ -177,6 +177,31 @@ def test_run_dm_loop_f32_engine_workload(engine, ref):
     assert abs(best["dm"] - 100.0) <= 2.0 and abs(int(best["peak_sample"]) - 2000) <= 4
 
 
+@pytest.mark.parametrize("window", [2001, 40001])
+def test_f32_baseline_exact_and_replayed_rows(engine, ref, monkeypatch, window):
+    """Float chunk of multiples of 1/8 (every trial's window sums exact in double -> the
+    fixed-point baseline) with one fine-grained sample late in the zero-delay channel:
+    trials short enough to exclude it stay exact, the rest take the sequential replay.
+    Both mixes, and the all-sequential baseline, match the reference library."""
+    hdr, plan, data = _small_u8_case()
+    g = data.astype(np.float32) / np.float32(8.0)
+    L = g.shape[0]
+    zero_ch = int(np.argmin(plan.delays[-1]))
+    g[L - 1 - 300, zero_ch] = np.float32(0.000123456)
+    md = np.array([plan.trial_max_delay(t) for t in range(plan.ntrials)])
+    assert (md > 300).any() and (md < 300).any()
+    cfg = EngineConfig(n_workers=2, tsamp=hdr.tsamp, boxcar_max=256, baseline_window=window, detect_thresh=5.0)
+    spec = ChunkSpec.whole(L)
+    want, want_sk, _ = ref.run_dm_loop(g, vars(spec), plan.dms, plan.delays, cfg_dict(cfg))
+    assert len(want) > 0
+    a = engine.run_dm_loop(Chunk(spec, g), plan, cfg)
+    monkeypatch.setenv("PGB_BASELINE_SERIAL", "1")
+    b = engine.run_dm_loop(Chunk(spec, g), plan, cfg)
+    for r in (a, b):
+        assert_same_candidates(r.candidates, want)
+        assert np.array_equal(r.skipped_trials, want_sk)
+
+
 def test_widened_u8_chunk_takes_integer_path(engine, port, monkeypatch):
     """A float chunk of 8-bit codes (read_chunk's widening) is repacked on the device;
     results equal the u8 path, the forced fp32 path and the oracle."""
