@@ -12,7 +12,10 @@
 //     (nth_element picks order statistics, so any exact selection agrees).
 //   * apply_mask (:93-139): zero or local-mean replacement computed from the
 //     original values, written into a separate float chunk.
+#include <cuda_pipeline.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cstdlib>
+#include <type_traits>
 
 #include "pgb_internal.h"
 
@@ -77,6 +80,139 @@ __global__ void zero_dm_kernel(const T* __restrict__ x, uint64_t n, uint32_t nch
         for (uint32_t cc = 0; cc < lim; ++cc) s = __dadd_rn(s, (double)tile[cc][tid]);
     }
     if (i0 + tid < n) zdm[i0 + tid] = s;
+}
+
+// ---- 8-bit chunks: integer sums are exact in any order -------------------------------
+// The reference's channel sums and zero-DM sums add doubles of 8-bit codes: every partial
+// sum is an integer < 2^53, so the result is the exact integer sum however it is formed.
+// Those two passes run HBM-parallel in integers; only the variance pass (an FMA chain whose
+// rounding depends on order) stays one sequential chain per channel, fed from shared
+// memory.  Fast paths need nch % 16 == 0 (16-byte rows); other shapes use the kernels above.
+__global__ void chan_sum_u8_kernel(const uint8_t* __restrict__ x, uint64_t n, uint32_t nch,
+                                   uint64_t rows_per, unsigned long long* __restrict__ sums) {
+    const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;  // channel quad
+    if (4 * q >= nch) return;
+    const uint64_t r0 = (uint64_t)blockIdx.y * rows_per;
+    const uint64_t r1 = r0 + rows_per < n ? r0 + rows_per : n;
+    uint32_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;  // rows_per <= 2^24
+    const uint32_t* src = reinterpret_cast<const uint32_t*>(x) + q;
+    const uint32_t pitch = nch / 4;
+#pragma unroll 8
+    for (uint64_t r = r0; r < r1; ++r) {
+        const uint32_t w = __ldg(src + r * pitch);
+        a0 += w & 0xffu;
+        a1 += (w >> 8) & 0xffu;
+        a2 += (w >> 16) & 0xffu;
+        a3 += w >> 24;
+    }
+    atomicAdd(sums + 4 * q + 0, (unsigned long long)a0);
+    atomicAdd(sums + 4 * q + 1, (unsigned long long)a1);
+    atomicAdd(sums + 4 * q + 2, (unsigned long long)a2);
+    atomicAdd(sums + 4 * q + 3, (unsigned long long)a3);
+}
+
+// one warp per sample row: zdm[i] = exact sum of the row's codes
+__global__ void zero_dm_u8_kernel(const uint8_t* __restrict__ x, uint64_t n, uint32_t nch,
+                                  double* __restrict__ zdm) {
+    const uint64_t row = ((uint64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (row >= n) return;
+    const uint4* src = reinterpret_cast<const uint4*>(x + row * nch);
+    uint32_t s = 0;
+    for (uint32_t v = lane; v < nch / 16; v += 32) {
+        const uint4 w = __ldg(src + v);
+        s = __dp4a(w.x, 0x01010101u, s);
+        s = __dp4a(w.y, 0x01010101u, s);
+        s = __dp4a(w.z, 0x01010101u, s);
+        s = __dp4a(w.w, 0x01010101u, s);
+    }
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) zdm[row] = (double)s;
+}
+
+// var[c] = sum_i fma chain of (x - mean)^2 in time order (src/rfi.cpp:48-52), one thread
+// per channel, 128 channels per CTA; rows staged 256 at a time through a 4-slot cp.async ring.
+constexpr int CV_CH = 128, CV_ROWS = 256, CV_NS = 4;
+
+__global__ void __launch_bounds__(CV_CH)
+    chan_var_u8_kernel(const uint8_t* __restrict__ x, uint64_t n, uint32_t nch,
+                       const unsigned long long* __restrict__ sums, double* __restrict__ mean,
+                       double* __restrict__ var) {
+    extern __shared__ __align__(16) uint8_t tile[];  // [CV_NS][CV_ROWS][CV_CH]
+    const uint32_t c0 = blockIdx.x * CV_CH;
+    const uint32_t cw = min((uint32_t)CV_CH, nch - c0);  // multiple of 16
+    const uint32_t parts = cw / 16;
+    const int tid = threadIdx.x;
+    const uint32_t c = c0 + tid;
+    const bool live = tid < (int)cw;
+    const double m = live ? __ddiv_rn((double)sums[c], (double)n) : 0.0;
+    const uint64_t nst = (n + CV_ROWS - 1) / CV_ROWS;
+    auto issue = [&](uint64_t k) {
+        if (k < nst) {
+            const uint64_t r0 = k * CV_ROWS;
+            const uint32_t rows = (uint32_t)min((uint64_t)CV_ROWS, n - r0);
+            uint8_t* dst = tile + (size_t)(k % CV_NS) * CV_ROWS * CV_CH;
+            for (uint32_t j = tid; j < rows * parts; j += CV_CH) {
+                const uint32_t r = j / parts, pp = j % parts;
+                __pipeline_memcpy_async(dst + r * CV_CH + 16 * pp, x + (r0 + r) * nch + c0 + 16 * pp, 16);
+            }
+        }
+        __pipeline_commit();
+    };
+    for (int k = 0; k < CV_NS - 1; ++k) issue(k);
+    double a = 0.0;
+    for (uint64_t k = 0; k < nst; ++k) {
+        __pipeline_wait_prior(CV_NS - 2);
+        __syncthreads();
+        issue(k + CV_NS - 1);  // into the slot stage k-1 used; everyone is past it
+        const uint8_t* t = tile + (size_t)(k % CV_NS) * CV_ROWS * CV_CH + tid;
+        const uint32_t rows = (uint32_t)min((uint64_t)CV_ROWS, n - k * CV_ROWS);
+        if (live) {
+            if (rows == CV_ROWS) {
+#pragma unroll 16
+                for (int r = 0; r < CV_ROWS; ++r) {
+                    const double d = __dsub_rn((double)t[r * CV_CH], m);
+                    a = __fma_rn(d, d, a);
+                }
+            } else {
+                for (uint32_t r = 0; r < rows; ++r) {
+                    const double d = __dsub_rn((double)t[r * CV_CH], m);
+                    a = __fma_rn(d, d, a);
+                }
+            }
+        }
+    }
+    if (live) {
+        mean[c] = m;
+        var[c] = __ddiv_rn(a, (double)n);
+    }
+}
+
+// widen to float with bad channels already zeroed (apply_mask's column rule), 4 cells a thread
+template <typename T>
+__global__ void widen_rows_kernel(const T* __restrict__ x, uint64_t n, uint32_t nch,
+                                  const uint8_t* __restrict__ chan_bad, float* __restrict__ out) {
+    const uint32_t q4 = nch / 4;
+    for (uint64_t r = blockIdx.x; r < n; r += gridDim.x) {
+        for (uint32_t q = threadIdx.x; q < q4; q += blockDim.x) {
+            const uint32_t bad = reinterpret_cast<const uint32_t*>(chan_bad)[q];
+            float4 v;
+            if constexpr (sizeof(T) == 1) {
+                const uint32_t w = __ldg(reinterpret_cast<const uint32_t*>(x + r * nch) + q);
+                v = make_float4((float)(w & 0xffu), (float)((w >> 8) & 0xffu), (float)((w >> 16) & 0xffu),
+                                (float)(w >> 24));
+            } else {
+                v = __ldg(reinterpret_cast<const float4*>(x + r * nch) + q);
+            }
+            if (bad) {
+                if (bad & 0xffu) v.x = 0.0f;
+                if (bad & 0xff00u) v.y = 0.0f;
+                if (bad & 0xff0000u) v.z = 0.0f;
+                if (bad & 0xff000000u) v.w = 0.0f;
+            }
+            reinterpret_cast<float4*>(out + r * nch)[q] = v;
+        }
+    }
 }
 
 __global__ void absdev_kernel(const double* __restrict__ v, uint64_t n,
@@ -204,13 +340,39 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
     if (rp.narrowband) {          // src/rfi.cpp:32-68
         if (nch < 4) raise(PGB_ERR_INSUFFICIENT, "narrowband flagging needs at least 4 channels");
         if (n == 0) raise(PGB_ERR_INSUFFICIENT, "empty chunk");
-        chan_stats_kernel<T><<<nblk(nch, 128), 128, 0, st>>>(x, n, nch, a, b);
+        if (std::is_same<T, uint8_t>::value && nch % 16 == 0 && !getenv("PGB_RFI_SERIAL")) {
+            auto* sums = reinterpret_cast<unsigned long long*>(s1);  // scratch until median_mad
+            PGB_CUDA(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * nch, st));
+            const uint32_t gx = (nch / 4 + 255) / 256;
+            uint64_t gy = std::max<uint64_t>(1, (148 * 16) / gx);
+            gy = std::max<uint64_t>(gy, (n + (1u << 24) - 1) >> 24);
+            gy = std::min<uint64_t>(gy, std::max<uint64_t>(1, n / 64));
+            const uint64_t rows_per = (n + gy - 1) / gy;
+            gy = (n + rows_per - 1) / rows_per;
+            chan_sum_u8_kernel<<<dim3(gx, (unsigned)gy), 256, 0, st>>>(
+                reinterpret_cast<const uint8_t*>(x), n, nch, rows_per, sums);
+            const size_t sm = (size_t)CV_NS * CV_ROWS * CV_CH;
+            static bool attr = false;
+            if (!attr) {
+                PGB_CUDA(cudaFuncSetAttribute(chan_var_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                              (int)sm));
+                attr = true;
+            }
+            chan_var_u8_kernel<<<(nch + CV_CH - 1) / CV_CH, CV_CH, sm, st>>>(reinterpret_cast<const uint8_t*>(x),
+                                                                           n, nch, sums, a, b);
+        } else {
+            chan_stats_kernel<T><<<nblk(nch, 128), 128, 0, st>>>(x, n, nch, a, b);
+        }
         median_mad(a, nch, stats, w.tmp, s1, s2, st);
         median_mad(b, nch, stats + 2, w.tmp, s1, s2, st);
         chan_flags_kernel<<<nblk(nch), 256, 0, st>>>(a, b, nch, stats, rp.k_mad, w.chan_bad.as<uint8_t>());
     }
     if (rp.broadband && n > 0) {  // src/rfi.cpp:70-91
-        zero_dm_kernel<T><<<nblk(n, 128), 128, 0, st>>>(x, n, nch, a);
+        if (std::is_same<T, uint8_t>::value && nch % 16 == 0 && !getenv("PGB_RFI_SERIAL"))
+            zero_dm_u8_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(reinterpret_cast<const uint8_t*>(x),
+                                                                                n, nch, a);
+        else
+            zero_dm_kernel<T><<<nblk(n, 128), 128, 0, st>>>(x, n, nch, a);
         median_mad(a, n, stats + 4, w.tmp, s1, s2, st);
         samp_flags_kernel<<<nblk(n), 256, 0, st>>>(a, n, stats + 4, rp.k_sigma, w.samp_bad.as<uint8_t>());
     }
@@ -228,7 +390,11 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
     for (auto v : cb) nbc += v;
     *n_bad_ch = nbc;
     *n_bad_s = nrows_bad;
-    widen_kernel<T><<<148 * 8, 256, 0, st>>>(x, cells, out);
+    const bool rows4 = nch % 4 == 0 && !getenv("PGB_RFI_SERIAL");
+    if (rows4)  // bad channels zeroed while widening
+        widen_rows_kernel<T><<<148 * 16, 256, 0, st>>>(x, n, nch, w.chan_bad.as<uint8_t>(), out);
+    else
+        widen_kernel<T><<<148 * 8, 256, 0, st>>>(x, cells, out);
     if (nbc == 0 && nrows_bad == 0) return;
     if (nrows_bad) {
         // the row list from atomics is unordered; each row is independent, so order is moot
@@ -236,7 +402,7 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
                                                             w.samp_bad.as<uint8_t>(), w.rows.as<uint64_t>(),
                                                             nrows_bad, rp.local_mean, out);
     }
-    if (nbc) {
+    if (nbc && !rows4) {
         dim3 g((unsigned)std::min<uint64_t>(n, 4096), (nch + 255) / 256);
         zero_channels_kernel<<<g, 256, 0, st>>>(n, nch, w.chan_bad.as<uint8_t>(), out);
     }

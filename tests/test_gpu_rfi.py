@@ -35,7 +35,9 @@ def _dirty_u8(L, nch, seed):
 
 
 @pytest.mark.parametrize("local_mean", [True, False])
-@pytest.mark.parametrize("L,nch", [(4096, 64), (20000, 256), (3000, 13)])
+# 16-byte rows take the integer-sum / staged-variance kernels (partial channel CTAs: 80,
+# 1040; partial row stages: 20000, 700); 36 widens 4 cells a thread only; 13 is all scalar
+@pytest.mark.parametrize("L,nch", [(4096, 64), (20000, 256), (3000, 13), (700, 80), (9000, 1040), (2500, 36)])
 def test_rfi_clean_u8_matches_reference(engine, ref, L, nch, local_mean):
     data = _dirty_u8(L, nch, seed=L + nch)
     want, wbc, wbs = ref.rfi(data.astype(np.float32), local_mean=local_mean)
