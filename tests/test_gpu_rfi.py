@@ -47,6 +47,17 @@ def test_rfi_clean_u8_matches_reference(engine, ref, L, nch, local_mean):
     assert np.array_equal(got.view(np.uint32), want.view(np.uint32))
 
 
+def test_rfi_scalar_kernels_agree(engine, ref, monkeypatch):
+    """PGB_RFI_SERIAL=1 (one thread per channel / sample, separate bad-channel pass) and the
+    default integer-sum kernels give identical flags and masked chunks."""
+    data = _dirty_u8(5000, 96, seed=11)
+    a = engine.rfi_clean(data, _plan(96), RfiConfig())
+    monkeypatch.setenv("PGB_RFI_SERIAL", "1")
+    b = engine.rfi_clean(data, _plan(96), RfiConfig())
+    for x, y in zip(a, b):
+        assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
+
+
 def test_rfi_clean_f32_matches_reference(engine, ref):
     rng = np.random.default_rng(3)
     L, nch = 6000, 48
