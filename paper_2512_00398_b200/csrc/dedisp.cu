@@ -304,14 +304,15 @@ constexpr int RING_NS = 3;
 // (mul.hi + mad.lo funnel) instead of PRMT on the ALU pipe; 2 = per-(channel, trial)
 // shared-memory addresses formed with IMAD (FMA pipe) instead of IADD (ALU pipe)
 // One (trial block, time tile) of the ring kernel; the whole CTA calls it.
-template <int G, int VPT, int MODE>
+template <int G, int VPT, int MODE, int NS = RING_NS>
 __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* __restrict__ rows,
                                           int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len,
                                           const uint32_t blk, const uint32_t tile) {
     constexpr int TPW = 2;
     constexpr int TB = DD_WARPS * TPW;
     static_assert(TB == 32, "table layout assumes 32-trial blocks");
-    constexpr int NS = RING_NS;
+    static_assert(NS == 2 || NS == 3, "ring depth");
+    constexpr uint32_t D = NS - 1;  // stages loaded ahead
     extern __shared__ __align__(16) uint8_t smem[];
     const uint32_t W = p.wmax;  // bytes per copy
     uint8_t* buf = smem;                                                           // [NS][G][4][W]
@@ -437,29 +438,29 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
         first_flush = false;
     };
 
-    // prologue: stages 0 and 1 into slots 0 and 1 (full phase 0 of each)
+    // prologue: stages 0 .. D-1 into slots 0 .. D-1 (full phase 0 of each)
     {
         const uint2 w0 = __ldg(wintab + my_cs);
         load_stage(0, w0);
         store_stage(0, w0);
-        if (nstages > 1) {
+        if (D > 1 && nstages > 1) {
             const uint2 w1 = __ldg(wintab + G + my_cs);
             load_stage(1, w1);
             store_stage(1, w1);
         }
     }
-    uint2 wnext = nstages > 2 ? __ldg(wintab + 2 * G + my_cs) : make_uint2(0, 0);
+    uint2 wnext = nstages > D ? __ldg(wintab + (size_t)D * G + my_cs) : make_uint2(0, 0);
     const uint32_t stages_per_flush = DD_FLUSH_CH / G;
     uint32_t since_flush = 0;
-    int slot = 0, slot2 = 2;          // gi % NS, (gi + 2) % NS
+    int slot = 0, slot2 = (int)D;     // gi % NS, (gi + D) % NS
     uint32_t ph = 0, ph_prev = 0;     // parity of stage gi's use of its slot; of stage gi-1's
 
     for (uint32_t gi = 0; gi < nstages; ++gi) {
-        const bool pre = gi + 2 < nstages;
+        const bool pre = gi + D < nstages;
         const uint2 wstage = wnext;
         if (pre) {
-            load_stage(gi + 2, wstage);
-            if (gi + 3 < nstages) wnext = __ldg(wintab + (size_t)(gi + 3) * G + my_cs);
+            load_stage(gi + D, wstage);
+            if (gi + D + 1 < nstages) wnext = __ldg(wintab + (size_t)(gi + D + 1) * G + my_cs);
         }
         ring_wait(full + slot, ph);
         const uint32_t* offb = offs + slot * G * TB + warp * TPW;
@@ -502,7 +503,7 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
     }
 }
 
-template <int G, int VPT, int MODE>
+template <int G, int VPT, int MODE, int NS = RING_NS>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_u8_ring_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
                           int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
@@ -510,13 +511,13 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     const uint32_t tile = blockIdx.y + p.tile0;
     if (p.blk_first && tile < p.blk_first[blk]) return;  // shifted in from the previous chunk
     if ((uint64_t)tile * DD_NT >= blk_len[blk]) return;
-    ring_tile<G, VPT, MODE>(p, rows, out, blk_len, blk, tile);
+    ring_tile<G, VPT, MODE, NS>(p, rows, out, blk_len, blk, tile);
 }
 
 // Persistent variant: one CTA per SM takes (block, tile) items from a counter in the
 // grid's order (blocks fastest), so the last wave is not quantised to whole CTAs of a
 // 7-55-wave grid (the tail is ~1 % of a launch with 8192 CTAs, several % with 1024).
-template <int G, int VPT>
+template <int G, int VPT, int NS = RING_NS>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_u8_ring_persist_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
                                   int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
@@ -532,7 +533,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
         const uint32_t blk = item % nblocks, tile = p.tile0 + item / nblocks;
         if (p.blk_first && tile < p.blk_first[blk]) continue;
         if ((uint64_t)tile * DD_NT >= blk_len[blk]) continue;
-        ring_tile<G, VPT, 0>(p, rows, out, blk_len, blk, tile);
+        ring_tile<G, VPT, 0, NS>(p, rows, out, blk_len, blk, tile);
     }
 }
 
@@ -1101,8 +1102,8 @@ int num_sms() {
     return n;
 }
 
-size_t ring_smem_bytes(int g, uint32_t wmax) {
-    return (size_t)RING_NS * g * 4 * wmax + (size_t)RING_NS * g * 32 * 4 + 2 * RING_NS * sizeof(uint64_t);
+size_t ring_smem_bytes(int g, uint32_t wmax, int ns = RING_NS) {
+    return (size_t)ns * g * 4 * wmax + (size_t)ns * g * 32 * 4 + 2 * ns * sizeof(uint64_t);
 }
 
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
@@ -1169,6 +1170,25 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
             PGB_RING(1, 1) PGB_RING(1, 2) PGB_RING(1, 4)
 #undef PGB_RING
 #undef PGB_RING3
+        }
+        // wide windows: a 2-slot ring at the double-buffered kernel's stage width (one
+        // stage of drift between warps instead of a CTA barrier per stage)
+        const size_t rsm2 = ring_smem_bytes(p.g, p.wmax, 2);
+        const uint32_t vstride2 = 32u * (DD_WARPS / p.g);
+        const int vpt2 = (int)((p.wmax / 16 + vstride2 - 1) / vstride2);
+        if (rmode == 0 && rsm2 <= 227 * 1024 && p.work_ctr && !getenv("PGB_DD_RING2_OFF")) {
+#define PGB_RING2(G_, V_)                                                                         \
+    if (p.g == G_ && vpt2 <= V_) {                                                                \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_, 2>,                   \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm2));   \
+        dedisp_u8_ring_persist_kernel<G_, V_, 2><<<num_sms(), DD_THREADS, rsm2, st>>>(p, rows, out, \
+                                                                                     p.blk_len);  \
+        PGB_CUDA(cudaGetLastError());                                                             \
+        return;                                                                                   \
+    }
+            PGB_RING2(8, 1) PGB_RING2(8, 2) PGB_RING2(8, 4)
+            PGB_RING2(4, 1) PGB_RING2(4, 2) PGB_RING2(4, 4)
+#undef PGB_RING2
         }
     }
     if (!v1 && p.tpw == 2 && p.dd_off) {

@@ -42,6 +42,7 @@ print("ok")
     {},                                   # persistent ring (u8), fp32 ring
     {"PGB_DD_PERSIST0": "1"},             # grid-launched ring
     {"PGB_DD_RING": "0"},                 # CTA-barrier table kernel
+    {"PGB_DD_RING2_OFF": "1"},            # wide windows: barrier kernel instead of the 2-slot ring
     {"PGB_RING_MODE": "2"},               # ring with IMAD addressing
     {"PGB_F32_RING0": "1"},               # fp32 two-barrier kernel
 ])
