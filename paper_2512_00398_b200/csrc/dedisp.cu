@@ -300,9 +300,13 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
 
 constexpr int RING_NS = 3;
 
-// MODE bits (ablation): 1 = byte shifts of the staged copies on the FMA pipe
-// (mul.hi + mad.lo funnel) instead of PRMT on the ALU pipe; 2 = per-(channel, trial)
-// shared-memory addresses formed with IMAD (FMA pipe) instead of IADD (ALU pipe)
+// MODE bits: 4 (default) = odd words accumulate K += (w >> 8) & 0x00ff00ff (one PRMT) and
+// T += w (IMAD), even words E += w & 0x00ff00ff (LOP3 + IMAD) and H += w >> 8 (LEA.HI): the
+// ALU and FMA pipes (equal rate) then carry 3 + 3 instructions per word pair instead of
+// 4 + 2.  Flush: B1 = K & 0xffff, B3 = K >> 16, T - 2^8 B1 - 2^24 B3 = B0 + 2^16 B2 (mod
+// 2^32, exact for <= 256 channels).  Ablations: 1 = byte shifts of the staged copies on
+// the FMA pipe (mul.hi + mad.lo funnel) instead of PRMT on the ALU pipe; 2 = per-(channel,
+// trial) shared-memory addresses formed with IMAD (FMA pipe) instead of IADD (ALU pipe)
 // One (trial block, time tile) of the ring kernel; the whole CTA calls it.
 template <int G, int VPT, int MODE, int NS = RING_NS>
 __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* __restrict__ rows,
@@ -418,9 +422,16 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
 #pragma unroll
                 for (int m = 0; m < DD_WORDS; ++m) {
                     const uint32_t e = E[u][m];
-                    const uint32_t b0 = e & 0xffffu, b2 = e >> 16;
-                    const uint32_t t = H[u][m] - (b2 << 8);  // B1 + 2^16 B3
-                    int4 val = make_int4((int)b0, (int)(t & 0xffffu), (int)b2, (int)(t >> 16));
+                    int4 val;
+                    if ((MODE & 4) && (m & 1)) {  // e = B1 + 2^16 B3, H = sum mod 2^32
+                        const uint32_t b1 = e & 0xffffu, b3 = e >> 16;
+                        const uint32_t r = H[u][m] - (b1 << 8) - (b3 << 24);  // B0 + 2^16 B2
+                        val = make_int4((int)(r & 0xffffu), (int)b1, (int)(r >> 16), (int)b3);
+                    } else {
+                        const uint32_t b0 = e & 0xffffu, b2 = e >> 16;
+                        const uint32_t t = H[u][m] - (b2 << 8);  // B1 + 2^16 B3
+                        val = make_int4((int)b0, (int)(t & 0xffffu), (int)b2, (int)(t >> 16));
+                    }
                     int4* pd = reinterpret_cast<int4*>(dst + 4 * (lane + 32 * m));
                     if (!first_flush) {
                         const int4 old = *pd;
@@ -478,10 +489,17 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
 #pragma unroll
                 for (int m = 0; m < DD_WORDS; ++m) {
                     const uint32_t w = *reinterpret_cast<const uint32_t*>(src + 128 * m);
-                    uint32_t e = E[u][m];
-                    asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(e) : "r"(w & 0x00ff00ffu), "r"(one));
+                    uint32_t e = E[u][m], h = H[u][m];
+                    if ((MODE & 4) && (m & 1)) {
+                        // K += bytes 1,3 in 16-bit lanes (one PRMT, ALU); T += w (IMAD, FMA pipe)
+                        asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(e) : "r"(__byte_perm(w, 0u, 0x4341)), "r"(one));
+                        asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(w), "r"(one));
+                    } else {
+                        asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(e) : "r"(w & 0x00ff00ffu), "r"(one));
+                        h += __umulhi(w, 1u << 24);  // LEA.HI, ALU pipe
+                    }
                     E[u][m] = e;
-                    H[u][m] += __umulhi(w, 1u << 24);  // LEA.HI, ALU pipe
+                    H[u][m] = h;
                 }
             }
         }
@@ -517,7 +535,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 // Persistent variant: one CTA per SM takes (block, tile) items from a counter in the
 // grid's order (blocks fastest), so the last wave is not quantised to whole CTAs of a
 // 7-55-wave grid (the tail is ~1 % of a launch with 8192 CTAs, several % with 1024).
-template <int G, int VPT, int NS = RING_NS>
+template <int G, int VPT, int NS = RING_NS, int MODE = 0>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_u8_ring_persist_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
                                   int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
@@ -533,7 +551,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
         const uint32_t blk = item % nblocks, tile = p.tile0 + item / nblocks;
         if (p.blk_first && tile < p.blk_first[blk]) continue;
         if ((uint64_t)tile * DD_NT >= blk_len[blk]) continue;
-        ring_tile<G, VPT, 0, NS>(p, rows, out, blk_len, blk, tile);
+        ring_tile<G, VPT, MODE, NS>(p, rows, out, blk_len, blk, tile);
     }
 }
 
@@ -1132,9 +1150,9 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const char* e = getenv("PGB_DD_RING");
         return !(e && *e == '0');
     }();
-    static const int rmode = [] {  // PGB_RING_MODE: ring-kernel ablation bits (see the kernel)
+    static const int rmode = [] {  // PGB_RING_MODE: ring accumulation / ablation bits (see the kernel)
         const char* e = getenv("PGB_RING_MODE");
-        return e ? atoi(e) & 3 : 0;
+        return e ? atoi(e) & 15 : 4;  // default: mixed ALU/FMA accumulation (4)
     }();
     if (ring && !v1 && !sf && p.tpw == 2 && p.dd_off) {
         int g = 8;
@@ -1142,52 +1160,55 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const size_t rsm = ring_smem_bytes(g, p.wmax);
         const uint32_t vstride = 32u * (DD_WARPS / g);
         const int vpt = (int)((p.wmax / 16 + vstride - 1) / vstride);
+        const bool pers = p.work_ctr && (rmode == 0 || rmode == 4);  // PGB_DD_PERSIST0 clears work_ctr
         // the 3-slot ring needs 1.5x the shared memory of the double-buffered kernel; when
-        // that forces fewer channels per stage (wide windows, e.g. config C) the
-        // barrier kernel with the larger stage is faster (18.4 vs 19.0 T adds/s on C)
+        // that forces fewer channels per stage (wide windows, e.g. config C) a 2-slot ring
+        // at the wider stage is faster (below; the 3-slot ring at G = 4: 18.4 T adds/s on C)
         if (rsm <= 227 * 1024 && g >= p.g) {
-#define PGB_RING3(G_, V_, M_)                                                                     \
-    if (g == G_ && vpt <= V_ && rmode == M_ && M_ == 0 && p.work_ctr) {                           \
-        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_>,                      \
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \
-        dedisp_u8_ring_persist_kernel<G_, V_><<<num_sms(), DD_THREADS, rsm, st>>>(p, rows, out,  \
-                                                                                 p.blk_len);      \
-        PGB_CUDA(cudaGetLastError());                                                             \
-        return;                                                                                   \
-    }                                                                                             \
+#define PGB_RINGK(G_, V_, M_)                                                                     \
     if (g == G_ && vpt <= V_ && rmode == M_) {                                                    \
-        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_kernel<G_, V_, M_>,                          \
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \
-        dedisp_u8_ring_kernel<G_, V_, M_><<<grid, DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len);\
+        if (pers) {                                                                               \
+            PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_, RING_NS, M_>,     \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm)); \
+            dedisp_u8_ring_persist_kernel<G_, V_, RING_NS, M_><<<num_sms(), DD_THREADS, rsm, st>>>( \
+                p, rows, out, p.blk_len);                                                         \
+        } else {                                                                                  \
+            PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_kernel<G_, V_, M_>,                      \
+                                          cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm)); \
+            dedisp_u8_ring_kernel<G_, V_, M_><<<grid, DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len); \
+        }                                                                                         \
         PGB_CUDA(cudaGetLastError());                                                             \
         return;                                                                                   \
     }
-#define PGB_RING(G_, V_) PGB_RING3(G_, V_, 0)
-            PGB_RING3(8, 2, 1) PGB_RING3(8, 2, 2) PGB_RING3(8, 2, 3)
+#define PGB_RING(G_, V_) PGB_RINGK(G_, V_, 0) PGB_RINGK(G_, V_, 4)
             PGB_RING(8, 1) PGB_RING(8, 2) PGB_RING(8, 4)
             PGB_RING(4, 1) PGB_RING(4, 2) PGB_RING(4, 4)
             PGB_RING(2, 1) PGB_RING(2, 2) PGB_RING(2, 4)
             PGB_RING(1, 1) PGB_RING(1, 2) PGB_RING(1, 4)
 #undef PGB_RING
-#undef PGB_RING3
+            // ablations (grid launch): 1 staging shifts on the FMA pipe, 2 IMAD addressing, 3 both
+            if (!pers) { PGB_RINGK(8, 2, 1) PGB_RINGK(8, 2, 2) PGB_RINGK(8, 2, 3) }
+#undef PGB_RINGK
         }
         // wide windows: a 2-slot ring at the double-buffered kernel's stage width (one
         // stage of drift between warps instead of a CTA barrier per stage)
         const size_t rsm2 = ring_smem_bytes(p.g, p.wmax, 2);
         const uint32_t vstride2 = 32u * (DD_WARPS / p.g);
         const int vpt2 = (int)((p.wmax / 16 + vstride2 - 1) / vstride2);
-        if (rmode == 0 && rsm2 <= 227 * 1024 && p.work_ctr && !getenv("PGB_DD_RING2_OFF")) {
-#define PGB_RING2(G_, V_)                                                                         \
-    if (p.g == G_ && vpt2 <= V_) {                                                                \
-        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_, 2>,                   \
+        if (pers && rsm2 <= 227 * 1024 && !getenv("PGB_DD_RING2_OFF")) {
+#define PGB_RING2(G_, V_, M_)                                                                     \
+    if (p.g == G_ && vpt2 <= V_ && rmode == M_) {                                                 \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_, 2, M_>,               \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm2));   \
-        dedisp_u8_ring_persist_kernel<G_, V_, 2><<<num_sms(), DD_THREADS, rsm2, st>>>(p, rows, out, \
-                                                                                     p.blk_len);  \
+        dedisp_u8_ring_persist_kernel<G_, V_, 2, M_><<<num_sms(), DD_THREADS, rsm2, st>>>(        \
+            p, rows, out, p.blk_len);                                                             \
         PGB_CUDA(cudaGetLastError());                                                             \
         return;                                                                                   \
     }
-            PGB_RING2(8, 1) PGB_RING2(8, 2) PGB_RING2(8, 4)
-            PGB_RING2(4, 1) PGB_RING2(4, 2) PGB_RING2(4, 4)
+            PGB_RING2(8, 1, 0) PGB_RING2(8, 2, 0) PGB_RING2(8, 4, 0)
+            PGB_RING2(4, 1, 0) PGB_RING2(4, 2, 0) PGB_RING2(4, 4, 0)
+            PGB_RING2(8, 1, 4) PGB_RING2(8, 2, 4) PGB_RING2(8, 4, 4)
+            PGB_RING2(4, 1, 4) PGB_RING2(4, 2, 4) PGB_RING2(4, 4, 4)
 #undef PGB_RING2
         }
     }
