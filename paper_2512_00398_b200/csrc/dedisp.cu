@@ -300,7 +300,9 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
 
 constexpr int RING_NS = 3;
 
-// MODE bits: 4 (default) = odd words accumulate K += (w >> 8) & 0x00ff00ff (one PRMT) and
+// MODE bits: 8 (default, G >= 2) = channel pairs, every word accumulated as K += PRMT(w0) +
+// PRMT(w1) (one IADD3) and T += w0, w1 (two IMADs): 2.5 instructions per word-add, ALU 1.5 /
+// FMA 1 (16 with 8: T by IADD3 on even words, ALU-heavier; ablation).  4 = odd words accumulate K += (w >> 8) & 0x00ff00ff (one PRMT) and
 // T += w (IMAD), even words E += w & 0x00ff00ff (LOP3 + IMAD) and H += w >> 8 (LEA.HI): the
 // ALU and FMA pipes (equal rate) then carry 3 + 3 instructions per word pair instead of
 // 4 + 2.  Flush: B1 = K & 0xffff, B3 = K >> 16, T - 2^8 B1 - 2^24 B3 = B0 + 2^16 B2 (mod
@@ -423,7 +425,7 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
                 for (int m = 0; m < DD_WORDS; ++m) {
                     const uint32_t e = E[u][m];
                     int4 val;
-                    if ((MODE & 4) && (m & 1)) {  // e = B1 + 2^16 B3, H = sum mod 2^32
+                    if (((MODE & 4) && (m & 1)) || ((MODE & 8) && G >= 2)) {  // e = B1 + 2^16 B3, H = sum mod 2^32
                         const uint32_t b1 = e & 0xffffu, b3 = e >> 16;
                         const uint32_t r = H[u][m] - (b1 << 8) - (b3 << 24);  // B0 + 2^16 B2
                         val = make_int4((int)(r & 0xffffu), (int)b1, (int)(r >> 16), (int)b3);
@@ -477,6 +479,32 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
         const uint32_t* offb = offs + slot * G * TB + warp * TPW;
         const uint8_t* bufb = buf + (size_t)slot * G * 4 * W + 4 * lane;
         const uint32_t bufo = (uint32_t)slot * G * 4 * W + 4 * lane;  // byte offset of bufb in smem
+        if constexpr ((MODE & 8) && G >= 2) {
+            // channel pairs, every word as (K, T): K += PRMT(w0) + PRMT(w1) (IADD3), T += w0,
+            // w1 (two IMADs; with MODE 16 one IADD3 on even words): 2.5 instructions per word
+#pragma unroll
+            for (int cs = 0; cs < G; cs += 2) {
+#pragma unroll
+                for (int u = 0; u < TPW; ++u) {
+                    const uint8_t* s0 = bufb + (size_t)cs * 4 * W + offb[cs * TB + u];
+                    const uint8_t* s1 = bufb + (size_t)(cs + 1) * 4 * W + offb[(cs + 1) * TB + u];
+#pragma unroll
+                    for (int m = 0; m < DD_WORDS; ++m) {
+                        const uint32_t w0 = *reinterpret_cast<const uint32_t*>(s0 + 128 * m);
+                        const uint32_t w1 = *reinterpret_cast<const uint32_t*>(s1 + 128 * m);
+                        uint32_t h = H[u][m];
+                        E[u][m] += __byte_perm(w0, 0u, 0x4341) + __byte_perm(w1, 0u, 0x4341);
+                        if ((MODE & 16) && !(m & 1)) {
+                            h += w0 + w1;
+                        } else {
+                            asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(w0), "r"(one));
+                            asm("mad.lo.u32 %0, %1, %2, %0;" : "+r"(h) : "r"(w1), "r"(one));
+                        }
+                        H[u][m] = h;
+                    }
+                }
+            }
+        } else
 #pragma unroll
         for (int cs = 0; cs < G; ++cs) {
 #pragma unroll
@@ -1152,7 +1180,7 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
     }();
     static const int rmode = [] {  // PGB_RING_MODE: ring accumulation / ablation bits (see the kernel)
         const char* e = getenv("PGB_RING_MODE");
-        return e ? atoi(e) & 15 : 4;  // default: mixed ALU/FMA accumulation (4)
+        return e ? atoi(e) & 31 : 8;  // default: channel-paired (K, T) accumulation (8)
     }();
     if (ring && !v1 && !sf && p.tpw == 2 && p.dd_off) {
         int g = 8;
@@ -1160,7 +1188,7 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const size_t rsm = ring_smem_bytes(g, p.wmax);
         const uint32_t vstride = 32u * (DD_WARPS / g);
         const int vpt = (int)((p.wmax / 16 + vstride - 1) / vstride);
-        const bool pers = p.work_ctr && (rmode == 0 || rmode == 4);  // PGB_DD_PERSIST0 clears work_ctr
+        const bool pers = p.work_ctr && (rmode == 0 || rmode == 4 || rmode == 8 || rmode == 24);  // PGB_DD_PERSIST0 clears work_ctr
         // the 3-slot ring needs 1.5x the shared memory of the double-buffered kernel; when
         // that forces fewer channels per stage (wide windows, e.g. config C) a 2-slot ring
         // at the wider stage is faster (below; the 3-slot ring at G = 4: 18.4 T adds/s on C)
@@ -1180,7 +1208,8 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         PGB_CUDA(cudaGetLastError());                                                             \
         return;                                                                                   \
     }
-#define PGB_RING(G_, V_) PGB_RINGK(G_, V_, 0) PGB_RINGK(G_, V_, 4)
+            PGB_RINGK(8, 1, 4) PGB_RINGK(8, 2, 4) PGB_RINGK(8, 4, 4) PGB_RINGK(8, 2, 24)
+#define PGB_RING(G_, V_) PGB_RINGK(G_, V_, 0) PGB_RINGK(G_, V_, 8)
             PGB_RING(8, 1) PGB_RING(8, 2) PGB_RING(8, 4)
             PGB_RING(4, 1) PGB_RING(4, 2) PGB_RING(4, 4)
             PGB_RING(2, 1) PGB_RING(2, 2) PGB_RING(2, 4)
@@ -1207,8 +1236,8 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
     }
             PGB_RING2(8, 1, 0) PGB_RING2(8, 2, 0) PGB_RING2(8, 4, 0)
             PGB_RING2(4, 1, 0) PGB_RING2(4, 2, 0) PGB_RING2(4, 4, 0)
-            PGB_RING2(8, 1, 4) PGB_RING2(8, 2, 4) PGB_RING2(8, 4, 4)
-            PGB_RING2(4, 1, 4) PGB_RING2(4, 2, 4) PGB_RING2(4, 4, 4)
+            PGB_RING2(8, 1, 8) PGB_RING2(8, 2, 8) PGB_RING2(8, 4, 8)
+            PGB_RING2(4, 1, 8) PGB_RING2(4, 2, 8) PGB_RING2(4, 4, 8)
 #undef PGB_RING2
         }
     }

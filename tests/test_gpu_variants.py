@@ -39,12 +39,14 @@ print("ok")
 
 
 @pytest.mark.parametrize("env", [
-    {},                                   # persistent ring (u8, mixed ALU/FMA accumulation), fp32 ring
+    {},                                   # persistent ring (u8, channel-paired K/T accumulation), fp32 ring
     {"PGB_DD_PERSIST0": "1"},             # grid-launched ring
     {"PGB_DD_RING": "0"},                 # CTA-barrier table kernel
     {"PGB_DD_RING2_OFF": "1"},            # wide windows: barrier kernel instead of the 2-slot ring
     {"PGB_RING_MODE": "2"},               # ring with IMAD addressing
     {"PGB_RING_MODE": "0"},               # persistent ring, every word accumulated as (LOP3, IMAD, LEA.HI)
+    {"PGB_RING_MODE": "4"},               # odd words as (PRMT, IMAD, IMAD), even words as mode 0
+    {"PGB_RING_MODE": "24"},              # channel pairs, T by IADD3 on even words
     {"PGB_F32_RING0": "1"},               # fp32 two-barrier kernel
 ])
 def test_dedispersion_variants_bit_exact(env):
