@@ -363,7 +363,7 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
                     "h2d_bytes_per_step": int(cfg["nsamples"] * cfg["nchans"]),
                     "d2h_bytes_per_step": int(d2h),
                     "x_realtime": (cfg["nsamples"] * cfg["tsamp"]) / (el_e2e / 1e3 / e2e_steps)},
-            "roofline": {"bound": "alu", "kernel": "dedisp_u8_ring_kernel",
+            "roofline": {"bound": "alu", "kernel": "dedisp_u8_ring_persist_kernel<8,2,3,8>",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tadd/s",
                          "frac": achieved / peak, "traffic": load_ncu_traffic(),
                          "per_unit": "nchans channel-adds per (trial, output sample)",
