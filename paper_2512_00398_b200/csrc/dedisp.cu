@@ -34,6 +34,8 @@
 #include <cstdlib>
 #include <type_traits>
 
+#include <cstdio>
+
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -1148,6 +1150,12 @@ int num_sms() {
     return n;
 }
 
+// PGB_DD_WHICH=1: print each u8 dedispersion launch's kernel choice to stderr (tests)
+void dd_which(const char* kind, int g, int vpt, int mode) {
+    static const bool on = getenv("PGB_DD_WHICH") != nullptr;
+    if (on) fprintf(stderr, "pgb dedisp: %s G=%d VPT=%d mode=%d\n", kind, g, vpt, mode);
+}
+
 size_t ring_smem_bytes(int g, uint32_t wmax, int ns = RING_NS) {
     return (size_t)ns * g * 4 * wmax + (size_t)ns * g * 32 * 4 + 2 * ns * sizeof(uint64_t);
 }
@@ -1205,6 +1213,7 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm)); \
             dedisp_u8_ring_kernel<G_, V_, M_><<<grid, DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len); \
         }                                                                                         \
+        dd_which(pers ? "ring3-persist" : "ring3-grid", G_, V_, M_);                              \
         PGB_CUDA(cudaGetLastError());                                                             \
         return;                                                                                   \
     }
@@ -1231,6 +1240,7 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm2));   \
         dedisp_u8_ring_persist_kernel<G_, V_, 2, M_><<<num_sms(), DD_THREADS, rsm2, st>>>(        \
             p, rows, out, p.blk_len);                                                             \
+        dd_which("ring2-persist", G_, V_, M_);                                                    \
         PGB_CUDA(cudaGetLastError());                                                             \
         return;                                                                                   \
     }
@@ -1250,6 +1260,7 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_tab_kernel<G_, V_, S_>,                           \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));   \
         dedisp_u8_tab_kernel<G_, V_, S_><<<grid, DD_THREADS, smem, st>>>(p, rows, out, p.blk_len);\
+        dd_which("barrier", G_, V_, S_);                                                          \
         PGB_CUDA(cudaGetLastError());                                                             \
         return;                                                                                   \
     }

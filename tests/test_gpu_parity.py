@@ -27,6 +27,8 @@ DEDISP_CASES = [
     # wide per-block delay spreads: 4 and 2 channels per stage, 3-4 vectors per stager
     (4096, 1518.0, -0.0703125, 24000, 800.0, 8.0),
     (4096, 1518.0, -0.0703125, 30000, 1400.0, 14.0),
+    # windows where three 8-channel ring slots do not fit but two do (2-slot ring)
+    (4096, 1518.0, -0.0703125, 20000, 400.0, 4.0),
     (1, 1500.0, -1.0, 2000, 0.0, 1.0),
     (517, 1450.0, -0.5, 12000, 400.0, 2.5),
 ]

@@ -54,3 +54,26 @@ def test_dedispersion_variants_bit_exact(env):
     out = subprocess.run([sys.executable, "-c", SNIPPET.format(root=str(ROOT))], env=e,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+
+
+WIDE = SNIPPET.replace(
+    "cases = [(4096, 1518.0, -0.0703125, 24000, 800.0, 8.0), (1024, 1500.0, -0.25, 20000, 500.0, 2.0),\n"
+    "         (517, 1450.0, -0.5, 12000, 400.0, 2.5)]",
+    "cases = [(4096, 1518.0, -0.0703125, 20000, 400.0, 4.0), (4096, 1518.0, -0.0703125, 16000, 300.0, 3.0),\n"
+    "         (1024, 1500.0, -0.25, 20000, 500.0, 2.0)]")
+
+
+@pytest.mark.parametrize("mode", ["", "0"])
+def test_default_selection_covers_both_ring_depths(mode):
+    """The default launcher picks the 3-slot ring for narrow windows and the 2-slot ring when
+    three slots would force narrower stages; both bit-exact (PGB_DD_WHICH logs the choice),
+    with the default and the per-word (mode 0) accumulation."""
+    assert WIDE != SNIPPET
+    e = dict(os.environ, PGB_DD_WHICH="1")
+    if mode:
+        e["PGB_RING_MODE"] = mode
+    out = subprocess.run([sys.executable, "-c", WIDE.format(root=str(ROOT))], env=e,
+                         capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
+    kinds = {line.split()[2] for line in out.stderr.splitlines() if line.startswith("pgb dedisp:")}
+    assert "ring3-persist" in kinds and "ring2-persist" in kinds, kinds
