@@ -204,6 +204,21 @@ def test_f32_baseline_exact_and_replayed_rows(engine, ref, monkeypatch, window):
         assert np.array_equal(r.skipped_trials, want_sk)
 
 
+def test_f32_baseline_subnormal_fixed_point(engine, ref):
+    """Every value a multiple of 2^-140 below 2^-126 (subnormal floats): the trials pass the
+    exactness check with L = -140 and run in fixed point; same candidates as the reference."""
+    hdr, plan, data = _small_u8_case()
+    g = (data.astype(np.float64) * 2.0 ** -140).astype(np.float32)
+    assert np.all(np.abs(g) < np.float32(2.0 ** -126))
+    cfg = EngineConfig(n_workers=2, tsamp=hdr.tsamp, boxcar_max=256, baseline_window=2001)
+    spec = ChunkSpec.whole(g.shape[0])
+    want, want_sk, _ = ref.run_dm_loop(g, vars(spec), plan.dms, plan.delays, cfg_dict(cfg))
+    assert len(want) > 0
+    res = engine.run_dm_loop(Chunk(spec, g), plan, cfg)
+    assert_same_candidates(res.candidates, want)
+    assert np.array_equal(res.skipped_trials, want_sk)
+
+
 def test_widened_u8_chunk_takes_integer_path(engine, port, monkeypatch):
     """A float chunk of 8-bit codes (read_chunk's widening) is repacked on the device;
     results equal the u8 path, the forced fp32 path and the oracle."""
