@@ -352,12 +352,8 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
             chan_sum_u8_kernel<<<dim3(gx, (unsigned)gy), 256, 0, st>>>(
                 reinterpret_cast<const uint8_t*>(x), n, nch, rows_per, sums);
             const size_t sm = (size_t)CV_NS * CV_ROWS * CV_CH;
-            static bool attr = false;
-            if (!attr) {
-                PGB_CUDA(cudaFuncSetAttribute(chan_var_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                              (int)sm));
-                attr = true;
-            }
+            // per call: the attribute is per device, and contexts may live on different GPUs
+            PGB_CUDA(cudaFuncSetAttribute(chan_var_u8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
             chan_var_u8_kernel<<<(nch + CV_CH - 1) / CV_CH, CV_CH, sm, st>>>(reinterpret_cast<const uint8_t*>(x),
                                                                            n, nch, sums, a, b);
         } else {
