@@ -5,31 +5,37 @@ Workload (config B, "Parkes-multibeam-like"): synthetic 8-bit filterbank, 4096
 channels, fch1 1518 MHz, foff -0.0703125 MHz, 64 us, 2^20 samples, DM 0-2000 step 2
 (1001 trials), boxcar widths 1..4096, baseline 2 s, threshold 6, 2^18-sample
 chunks (5 overlapping chunks, overlap = max_delay + boxcar_max), 10 injected
-pulses.  One step = the whole file through the hot path: every chunk's
-dedispersion + detection chain, the file-level candidate sort and link_grid.
+pulses.  The payload is tools/synth.py's deterministic host generator, so both arms
+and the golden parity fixtures (tests/golden/config_B.npz) see identical bytes.
+One step = the whole file through the hot path: every chunk's dedispersion +
+detection chain, the file-level candidate sort and link_grid.
 
   value : DM-trial*samples/s = ntrials * nsamples * steps / device time, payload
           resident in HBM (4 GiB > L2, so no L2 flush is needed between steps)
-  e2e   : the same through the C ABI from pinned host memory: the 4 GiB payload
-          H2D (copy stream, overlapped) and the candidate/cluster D2H are inside
-          every timed step
-  roofline : the dominant kernel (dedispersion) is CUDA-core-ALU bound (~460
-          channel-adds per algorithmic byte): achieved channel-adds/s over the
-          measured 32-bit add peak of this GPU (pgb_microbench_add_peak)
-  cpu_baseline : the reference library (oracle/_ref, compiled from the reference's
-          own sources) in parity mode on the host cores, on a bounded sample
+  e2e   : the same with the input crossing the host link inside every step: one GPU
+          searches the pinned host payload through the C ABI (4 GiB H2D on a copy
+          stream, overlapped); N GPUs each upload 1/N of the rows and pull the rest from
+          their peers over NVLink (CUDA IPC).  Candidate/cluster D2H inside every step.
+  roofline : the dominant kernel (dedispersion) is CUDA-core bound (~460 channel-adds
+          per algorithmic byte): achieved channel-adds/s over the measured 32-bit add
+          peak of this GPU (pgb_microbench_add_peak); smem_frac against the
+          shared-memory ceiling of one byte per add (128 B/clk/SM)
+  cpu_baseline : the reference library (oracle/_ref, compiled from the reference's own
+          sources) in parity mode on all host threads, on chunk 0 with every 4th trial
 
-`--impl reference` times only the reference CPU implementation (rank 0).
-Multi-GPU (torchrun, one rank per GPU): DM trials are sharded across ranks, the
-candidate lists are gathered with NCCL and rank 0 clusters them (strong scaling:
-the file is fixed, each rank does 1/N of the trials).
+`--impl reference` times only the reference CPU implementation (rank 0): its own
+generate_dm_trials / create_task chunk plan, the same payload bytes, the same sample
+as cpu_baseline; it never loads the product library.
+`--gpus N` (N > 1) re-launches itself under torch.distributed.run with N ranks, one
+per GPU: DM trials are sharded across ranks, candidate lists gathered with NCCL and
+rank 0 clusters them (strong scaling: the file is fixed).
 """
 from __future__ import annotations
 
 import argparse
 import json
-import math
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -42,88 +48,112 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-CONFIG_B = dict(workload="config_B_parkes_like", nchans=4096, fch1=1518.0, foff=-0.0703125,
-                tsamp=64e-6, nsamples=1 << 20, dm_lo=0.0, dm_hi=2000.0, dm_step=2.0,
-                boxcar_max=4096, detect_thresh=6.0, baseline_s=2.0, nsamps_chunk=1 << 18,
-                npulses=10, seed=1001)
+from tools import synth  # noqa: E402  (host-side data generator, no product import)
+
+CONFIG_B = dict(synth.CONFIGS["B"])
 METRIC = "DM-trial*samples/s"
+REF_TRIAL_STRIDE = 4  # cpu sample: every 4th trial of chunk 0 (identical in both CPU legs)
 
 
 def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
-# ---- synthetic data ------------------------------------------------------------------
-
-def _noise_table() -> np.ndarray:
-    """u16 random -> N(100, 16^2) quantised round-half-up to u8 (inverse CDF table)."""
-    from statistics import NormalDist
-
-    nd = NormalDist(100.0, 16.0)
-    u = (np.arange(65536) + 0.5) / 65536.0
-    x = np.array([nd.inv_cdf(v) for v in u])
-    return np.clip(np.floor(x + 0.5), 0, 255).astype(np.uint8)
-
-
-def pulse_specs(cfg, plan):
-    """(trial, t0, width, snr) of the injected pulses, spread over DM, time and width."""
-    rng = np.random.default_rng(cfg["seed"])
-    out = []
-    n = cfg["npulses"]
-    for k in range(n):
-        trial = int((k + 0.5) / n * (plan.ntrials - 1))
-        width = 1 << int(rng.integers(0, 8))
-        snr = float(rng.uniform(12.0, 20.0))
-        span = cfg["nsamples"] - int(plan.delays[trial].max()) - width - 1
-        t0 = int((k + 0.5) / n * span)
-        out.append((trial, t0, width, snr))
-    return out
+def config_block(cfg, ntrials: int, nchunks: int, world: int) -> dict:
+    """The `config` object of both arms' JSON lines (identical for the same workload)."""
+    return {"workload": cfg["workload"], "nchans": cfg["nchans"], "nsamples": cfg["nsamples"],
+            "ntrials": ntrials, "dm": f"{cfg['dm_lo']}-{cfg['dm_hi']} step {cfg['dm_step']}",
+            "boxcar_max": cfg["boxcar_max"], "baseline_s": cfg["baseline_s"],
+            "nsamps_chunk": cfg["nsamps_chunk"], "chunks": nchunks,
+            "parallelism": f"dm-trial shards x{world}",
+            "l2": "inputs larger than L2 (4 GiB payload, 1 GiB chunks)",
+            "payload": "tools/synth.py seed %d (sha256-pinned in tests/golden/config_B.npz)" % cfg["seed"]}
 
 
-def make_payload(cfg, plan, rows: int | None = None, device: str = "cuda"):
-    """[rows][nchans] uint8 torch tensor (default: the whole file) on `device`."""
-    import torch
-
-    rows = rows or cfg["nsamples"]
-    nch = cfg["nchans"]
-    table = torch.from_numpy(_noise_table()).to(device)
-    g = torch.Generator(device=device)
-    g.manual_seed(cfg["seed"])
-    out = torch.empty((rows, nch), dtype=torch.uint8, device=device)
-    step = 1 << 14
-    for r0 in range(0, rows, step):
-        r1 = min(rows, r0 + step)
-        idx = torch.randint(0, 65536, ((r1 - r0) * nch,), generator=g, device=device, dtype=torch.int32)
-        out[r0:r1] = table[idx].view(r1 - r0, nch)
-    chans = torch.arange(nch, device=device)
-    for trial, t0, width, snr in pulse_specs(cfg, plan):
-        amp = snr * 16.0 / math.sqrt(nch * width)
-        d = torch.from_numpy(plan.delays[trial]).to(device)
-        for w in range(width):
-            r = t0 + d + w
-            keep = r < rows
-            rr, cc = r[keep], chans[keep]
-            v = out[rr, cc].to(torch.float32) + amp
-            out[rr, cc] = torch.clamp(torch.floor(v + 0.5), 0, 255).to(torch.uint8)
-    return out
+def host_cpu_info() -> dict:
+    info = {"model": None, "physical_cores": None, "logical_cpus": os.cpu_count(),
+            "usable_cpus": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        cps, sockets = int(kv.get("Core(s) per socket", 0)), int(kv.get("Socket(s)", 0))
+        info["physical_cores"] = cps * sockets or None
+    except (OSError, ValueError, subprocess.SubprocessError):
+        pass
+    return info
 
 
-def build_task(cfg):
-    from paper_2512_00398_b200.dedisp import FilterbankHeader, LinearSpacing
-    from paper_2512_00398_b200.engine import EngineConfig, RfiConfig
-    from paper_2512_00398_b200.pipeline import SearchParams, create_task
+# ---- CPU reference (oracle/_ref: the unmodified reference library) --------------------------
 
-    hdr = FilterbankHeader(fch1=cfg["fch1"], foff=cfg["foff"], nchans=cfg["nchans"],
-                           tsamp=cfg["tsamp"], nsamples=cfg["nsamples"])
-    params = SearchParams(dm_lo=cfg["dm_lo"], dm_hi=cfg["dm_hi"], spacing=LinearSpacing(cfg["dm_step"]),
-                          engine=EngineConfig(n_workers=1, detect_thresh=cfg["detect_thresh"],
-                                              boxcar_max=cfg["boxcar_max"]),
-                          baseline_len_s=cfg["baseline_s"], nsamps_chunk=cfg["nsamps_chunk"],
-                          rfi=RfiConfig(narrowband=cfg.get("rfi", False), broadband=cfg.get("rfi", False)))
-    return create_task(hdr, params)
+def reference_plan(ref, cfg):
+    """The reference's own DM plan and create_task chunk plan / baseline window for the
+    workload (create_task reads nsamples from the file size, so a sparse file of the
+    right size stands in for the payload)."""
+    dms, delays = ref.generate_dm_trials(cfg["dm_lo"], cfg["dm_hi"], cfg["fch1"], cfg["foff"], cfg["tsamp"],
+                                         cfg["nchans"], step=cfg["dm_step"])
+    with tempfile.TemporaryDirectory() as td:
+        path = Path(td) / "sparse.fil"
+        with open(path, "wb") as f:
+            f.write(synth.header_bytes(cfg))
+            f.truncate(len(synth.header_bytes(cfg)) + cfg["nsamples"] * cfg["nchans"])
+        chunks, bw = ref.create_task_plan(path, dm_lo=cfg["dm_lo"], dm_hi=cfg["dm_hi"], dm_step=cfg["dm_step"],
+                                          boxcar_max=cfg["boxcar_max"], baseline_len_s=cfg["baseline_s"],
+                                          nsamps_chunk=cfg["nsamps_chunk"])
+    return dms, delays, chunks, bw
 
 
-# ---- clocks ------------------------------------------------------------------------------
+def reference_sample(ref, cfg, dms, delays, spec, bw: int, chunk0: np.ndarray, threads: int):
+    """run_dm_loop of the reference (parity mode, `threads` workers) on chunk 0 with every
+    REF_TRIAL_STRIDE-th trial.  Returns (rate, wall_s, sample description)."""
+    trials = np.arange(0, len(dms), REF_TRIAL_STRIDE)
+    ecfg = dict(n_workers=threads, tsamp=cfg["tsamp"], detect_thresh=cfg["detect_thresh"],
+                boxcar_max=cfg["boxcar_max"], baseline_window=bw)
+    _, _, ms = ref.run_dm_loop(chunk0, spec, dms[trials], delays[trials], ecfg, parity=True)
+    valid = int(spec["valid_end"]) - int(spec["valid_begin"])
+    useful = len(trials) * valid
+    desc = (f"chunk 0 of {cfg['workload']} ({int(spec['length'])} samples, valid {valid}), "
+            f"{len(trials)} of {len(dms)} trials (every {REF_TRIAL_STRIDE}th), run_dm_loop in parity mode "
+            f"(max_in_flight = n_workers = {threads}); includes the reference's per-chunk transpose")
+    return useful / (ms / 1e3), ms / 1e3, desc
+
+
+def run_reference_arm(args, cfg, rank: int):
+    if rank != 0:
+        return
+    from oracle.pyoracle import Reference
+
+    ref = Reference()
+    dms, delays, chunks, bw = reference_plan(ref, cfg)
+    threads = len(os.sched_getaffinity(0))
+    spec = chunks[0]
+    chunk0 = synth.payload(cfg, delays, 0, int(spec["length"]))
+    for _ in range(args.warmup):
+        reference_sample(ref, cfg, dms, delays, spec, bw, chunk0, threads)
+    rates, walls, desc = [], [], ""
+    for _ in range(args.steps):
+        r, w, desc = reference_sample(ref, cfg, dms, delays, spec, bw, chunk0, threads)
+        rates.append(r)
+        walls.append(w)
+    value = sum(r * w for r, w in zip(rates, walls)) / sum(walls)
+    cpu = host_cpu_info()
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "DM-trial*samples/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * sum(walls) / len(walls), "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32 (reference fp32 dedispersion), fp64 detection",
+        "data": "synthetic", "config": config_block(cfg, len(dms), len(chunks), args.gpus),
+        "cpu_baseline": {"value": value, "unit": "DM-trial*samples/s", "cores": threads, "kind": "reference",
+                         "sample": desc, "cpu": cpu},
+        "e2e": {"value": value, "unit": "DM-trial*samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "x_realtime": value / len(dms) * cfg["tsamp"],
+    }
+    print(json.dumps(line), flush=True)
+
 
 class ClockSampler:
     QUERY = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
@@ -170,67 +200,6 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(rows)}
 
 
-# ---- CPU reference ------------------------------------------------------------------------
-
-def reference_sample(cfg, plan, task, payload_chunk0: np.ndarray, target_s: float, threads: int):
-    """Time the reference run_dm_loop (parity mode) on chunk 0 over a strided trial
-    subset sized to ~target_s of CPU work.  Returns (rate, wall_s, sample_desc)."""
-    from oracle.pyoracle import Reference
-
-    ref = Reference()
-    spec = task.chunks[0]
-    L = spec.length
-    # ~ channel-adds per second of the reference on `threads` cores (SURVEY.md section 6)
-    est_rate = 1.2e9 * threads
-    per_trial = L * cfg["nchans"]
-    ntr = int(max(4, min(plan.ntrials, target_s * est_rate / per_trial)))
-    stride = max(1, plan.ntrials // ntr)
-    trials = np.arange(0, plan.ntrials, stride)[:ntr]
-    dms, delays = plan.dms[trials], plan.delays[trials]
-    ecfg = dict(n_workers=threads, tsamp=cfg["tsamp"], detect_thresh=cfg["detect_thresh"],
-                boxcar_max=cfg["boxcar_max"], baseline_window=task.engine.baseline_window)
-    cands, skipped, ms = ref.run_dm_loop(payload_chunk0, vars(spec), dms, delays, ecfg, parity=True)
-    useful = len(trials) * (spec.valid_end - spec.valid_begin)
-    desc = (f"chunk 0 of {cfg['workload']} ({L} samples, valid {spec.valid_end - spec.valid_begin}), "
-            f"{len(trials)} of {plan.ntrials} trials (every {stride}th), parity mode, {threads} threads")
-    return useful / (ms / 1e3), ms / 1e3, desc
-
-
-def run_reference_arm(args, cfg, rank: int):
-    if rank != 0:
-        return
-    from paper_2512_00398_b200.dedisp import generate_dm_trials  # noqa: F401  (plan only)
-
-    task = build_task(cfg)
-    plan = task.plan
-    threads = os.cpu_count() or 1
-    chunk0 = make_payload(cfg, plan, rows=task.chunks[0].length, device="cpu").numpy()
-    per_step = float(os.environ.get("PG_REF_STEP_S", "8.0"))
-    for _ in range(args.warmup):
-        reference_sample(cfg, plan, task, chunk0, per_step, threads)
-    rates, walls, desc = [], [], ""
-    for _ in range(args.steps):
-        r, w, desc = reference_sample(cfg, plan, task, chunk0, per_step, threads)
-        rates.append(r)
-        walls.append(w)
-    total_units = sum(r * w for r, w in zip(rates, walls))
-    value = total_units / sum(walls)
-    line = {
-        "impl": "reference", "metric": METRIC, "value": value, "unit": "DM-trial*samples/s",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": 1e3 * sum(walls) / len(walls), "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["workload"], "nchans": cfg["nchans"], "nsamples": cfg["nsamples"],
-                   "ntrials": plan.ntrials, "boxcar_max": cfg["boxcar_max"],
-                   "parallelism": f"{threads} host threads"},
-        "cpu_baseline": {"value": value, "unit": "DM-trial*samples/s", "cores": threads,
-                         "kind": "reference", "sample": desc},
-        "e2e": {"value": value, "unit": "DM-trial*samples/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
-        "x_realtime": value / plan.ntrials * cfg["tsamp"],
-    }
-    print(json.dumps(line), flush=True)
-
 
 # ---- our arm ------------------------------------------------------------------------------
 
@@ -244,11 +213,40 @@ def load_ncu_traffic() -> float | None:
     return None
 
 
+def make_payload(cfg, plan, rows: int | None = None, device: str = "cuda"):
+    """[rows][nchans] uint8 torch tensor of the config's payload (tools/synth.py bytes,
+    RFI included when the config asks for it) on `device` (tools and tests)."""
+    import torch
+
+    host = torch.from_numpy(synth.payload(cfg, plan.delays, 0, rows or cfg["nsamples"]))
+    return host if device == "cpu" else host.to(device)
+
+
+def pulse_specs(cfg, plan):
+    return synth.pulse_specs(cfg, plan.delays)
+
+
+def build_task(cfg):
+    from paper_2512_00398_b200.dedisp import FilterbankHeader, LinearSpacing
+    from paper_2512_00398_b200.engine import EngineConfig, RfiConfig
+    from paper_2512_00398_b200.pipeline import SearchParams, create_task
+
+    hdr = FilterbankHeader(fch1=cfg["fch1"], foff=cfg["foff"], nchans=cfg["nchans"],
+                           tsamp=cfg["tsamp"], nsamples=cfg["nsamples"])
+    rfi = bool(cfg.get("rfi", False))
+    params = SearchParams(dm_lo=cfg["dm_lo"], dm_hi=cfg["dm_hi"], spacing=LinearSpacing(cfg["dm_step"]),
+                          engine=EngineConfig(n_workers=1, detect_thresh=cfg["detect_thresh"],
+                                              boxcar_max=cfg["boxcar_max"]),
+                          baseline_len_s=cfg["baseline_s"], nsamps_chunk=cfg["nsamps_chunk"],
+                          rfi=RfiConfig(narrowband=rfi, broadband=rfi))
+    return create_task(hdr, params)
+
+
 def run_ours(args, cfg, rank: int, world: int, local_rank: int):
     import torch
 
-    from paper_2512_00398_b200 import _native
-    from paper_2512_00398_b200.distributed import DD_TRIAL_BLOCK, gather_candidates, shard_trials, trial_work
+    from paper_2512_00398_b200.distributed import (DD_TRIAL_BLOCK, PayloadFanout, gather_candidates,
+                                                   shard_trials, trial_work)
     from paper_2512_00398_b200.engine import Engine
 
     # PG_DIST_BACKEND=gloo + PG_SAME_GPU=1 exercise the multi-rank path on one GPU
@@ -267,116 +265,156 @@ def run_ours(args, cfg, rank: int, world: int, local_rank: int):
             dist.init_process_group(backend)
     task = build_task(cfg)
     plan = task.plan
-    t0 = time.time()
-    payload = make_payload(cfg, plan, device=f"cuda:{local_rank}")
-    torch.cuda.synchronize()
-    log(f"[rank {rank}] payload {tuple(payload.shape)} generated in {time.time() - t0:.1f}s; "
-        f"{len(task.chunks)} chunks, {plan.ntrials} trials, baseline window {task.engine.baseline_window}")
-    lo, hi = shard_trials(trial_work(plan, [c.length for c in task.chunks]), world, DD_TRIAL_BLOCK)[rank]
+    nsamples, nch = cfg["nsamples"], cfg["nchans"]
     eng = Engine(local_rank)
-    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=f"cuda:{local_rank}")
     dev = torch.device("cuda", local_rank)
+    gdev = dev if backend == "nccl" else torch.device("cpu")
+    stream = torch.cuda.ExternalStream(eng.stream_handle(), device=dev)
 
-    def step(src, on_host: bool):
-        """One file through the hot path; returns (d2h bytes, dedisp ms, dedisp launches, adds)."""
-        cands, clusters, _ = eng.search_file(src, cfg["nsamples"], task.chunks, plan, task.engine,
+    # host payload (pinned): the whole file on one GPU, this rank's 1/N of the rows on N
+    t0 = time.time()
+    fan = None
+    if world == 1:
+        host_t = torch.empty((nsamples, nch), dtype=torch.uint8, pin_memory=True)
+        host = host_t.numpy()
+        synth.payload(cfg, plan.delays, out=host)
+        dev_payload = torch.empty((nsamples, nch), dtype=torch.uint8, device=dev)
+        dev_payload.copy_(host_t)
+        torch.cuda.synchronize()
+    else:
+        fan = PayloadFanout(eng, nsamples, nch)
+        r0, r1 = fan.own_rows
+        host_t = torch.empty((r1 - r0, nch), dtype=torch.uint8, pin_memory=True)
+        host = host_t.numpy()
+        synth.payload(cfg, plan.delays, r0, r1 - r0, out=host)
+        fan.upload_own(host)
+        fan.exchange()
+        eng.synchronize()
+        dev_payload = fan.buf
+    log(f"[rank {rank}] payload rows {nsamples if world == 1 else fan.own_rows} generated + resident in "
+        f"{time.time() - t0:.1f}s; {len(task.chunks)} chunks, {plan.ntrials} trials, "
+        f"baseline window {task.engine.baseline_window}")
+    lo, hi = shard_trials(trial_work(plan, [c.length for c in task.chunks]), world, DD_TRIAL_BLOCK)[rank]
+
+    def step(src):
+        """One file through the hot path; returns (h2d bytes, d2h bytes, dedisp ms, launches, adds)."""
+        h2d = 0
+        if src == "host" and fan is not None:  # 1/N of the rows from host memory, the rest over NVLink
+            h2d = fan.upload_own(host)
+            fan.exchange()
+            payload = fan.buf
+        elif src == "host":
+            h2d = host.nbytes
+            payload = host
+        else:
+            payload = dev_payload
+        cands, clusters, _ = eng.search_file(payload, nsamples, task.chunks, plan, task.engine,
                                              trial_range=(lo, hi), cluster=(world == 1))
         d2h = cands.nbytes + (clusters.records.nbytes + clusters.members.nbytes if world == 1 else 0)
         if world > 1:
-            merged = gather_candidates(cands, device=dev if backend == "nccl" else torch.device("cpu"))
+            merged = gather_candidates(cands, device=gdev)
             if rank == 0:
                 cl = eng.link_grid(merged, task.engine.radii)
                 d2h += cl.records.nbytes + cl.members.nbytes
         ms, nl, adds = eng.last_dedisp_time()
-        return d2h, ms, nl, adds
+        return h2d, d2h, ms, nl, adds
 
-    def timed(src, on_host: bool, steps: int):
+    def timed(src, steps: int):
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
         launches0 = eng.launch_count()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         ev0.record(stream)
-        d2h = 0
-        dd_ms = dd_n = dd_adds = 0
+        tot = np.zeros(5)
         for _ in range(steps):
-            b, ms, nl, adds = step(src, on_host)
-            d2h += b
-            dd_ms += ms
-            dd_n += nl
-            dd_adds += adds
+            tot += np.array(step(src), dtype=np.float64)
         ev1.record(stream)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
         el = ev0.elapsed_time(ev1)
         if dist:
-            t = torch.tensor([el], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+            t = torch.tensor([el], dtype=torch.float64, device=gdev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             el = float(t.item())
-        return el, d2h // steps, eng.launch_count() - launches0, dd_ms, dd_n, dd_adds
+        return el, eng.launch_count() - launches0, tot
 
     for _ in range(args.warmup):
-        step(payload, False)
+        step("device")
     with ClockSampler(local_rank) as clk:
-        el, _, launches, dd_ms, dd_n, dd_adds = timed(payload, False, args.steps)
-    units = plan.ntrials * cfg["nsamples"] * args.steps
+        el, launches, tot = timed("device", args.steps)
+    units = plan.ntrials * nsamples * args.steps
     value = units / (el / 1e3)
+    dd_ms, dd_n, dd_adds = tot[2], tot[3], tot[4]
 
-    # e2e through the C ABI from pinned host memory (H2D + D2H inside every step)
-    host = payload.cpu().pin_memory()
-    step(host, True)
+    # e2e: the input crosses the host link inside every step
+    step("host")
     e2e_steps = max(1, min(args.steps, 5))
-    el_e2e, d2h, _, _, _, _ = timed(host, True, e2e_steps)
-    e2e_value = plan.ntrials * cfg["nsamples"] * e2e_steps / (el_e2e / 1e3)
+    el_e2e, _, tot_e2e = timed("host", e2e_steps)
+    e2e_value = plan.ntrials * nsamples * e2e_steps / (el_e2e / 1e3)
+    h2d_step = tot_e2e[0] / e2e_steps
+    d2h_step = tot_e2e[1] / e2e_steps
+    if dist:  # whole-job host traffic: every rank's slice
+        t = torch.tensor([h2d_step], dtype=torch.float64, device=gdev)
+        dist.all_reduce(t)
+        h2d_step = float(t.item())
 
-    # roofline of the dominant kernel
     peak = _native_add_peak(local_rank)
     per_launch_ms = dd_ms / max(1, dd_n)
     achieved = (dd_adds / max(1, dd_n)) / (per_launch_ms / 1e3)
+    clocks = clk.summary()
     result = None
     if rank == 0:
         cpu = None
         if world == 1 and not args.no_cpu_baseline:
             try:
-                chunk0 = payload[: task.chunks[0].length].cpu().numpy()
-                threads = os.cpu_count() or 1
-                rate, wall, desc = reference_sample(cfg, plan, task, chunk0, args.cpu_seconds, threads)
-                cpu = {"value": rate, "unit": "DM-trial*samples/s", "cores": threads,
-                       "kind": "reference", "sample": desc, "wall_s": wall}
-            except Exception as exc:  # the oracle is optional on a box without oracle/_ref
+                from oracle.pyoracle import Reference
+
+                ref = Reference()
+                spec0 = task.chunks[0]
+                spec = dict(index=spec0.index, start_sample=spec0.start_sample, length=spec0.length,
+                            overlap=spec0.overlap, valid_begin=spec0.valid_begin, valid_end=spec0.valid_end)
+                threads = len(os.sched_getaffinity(0))
+                rate, wall, desc = reference_sample(ref, cfg, plan.dms, plan.delays, spec,
+                                                    task.engine.baseline_window, host[: spec0.length], threads)
+                cpu = {"value": rate, "unit": "DM-trial*samples/s", "cores": threads, "kind": "reference",
+                       "sample": desc, "wall_s": wall, "cpu": host_cpu_info()}
+            except Exception as exc:  # the checker is optional on a box without oracle/_ref
                 log(f"cpu baseline unavailable: {exc}")
+        sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+        smem_peak = 128.0 * 148 * sm_hz  # one shared-memory byte per channel-add
         result = {
             "metric": METRIC, "value": value, "unit": "DM-trial*samples/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": el / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int32 (u8 SWAR dedispersion), fp64 detection", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "nchans": cfg["nchans"],
-                       "nsamples": cfg["nsamples"], "ntrials": plan.ntrials,
-                       "dm": f"{cfg['dm_lo']}-{cfg['dm_hi']} step {cfg['dm_step']}",
-                       "boxcar_max": cfg["boxcar_max"], "baseline_s": cfg["baseline_s"],
-                       "nsamps_chunk": cfg["nsamps_chunk"], "chunks": len(task.chunks),
-                       "parallelism": f"dm-trial shards x{world}",
-                       "l2": "inputs larger than L2 (4 GiB payload, 1 GiB chunks)"},
-            "x_realtime": (cfg["nsamples"] * cfg["tsamp"]) / (el / 1e3 / args.steps),
-            "e2e": {"value": e2e_value, "unit": "DM-trial*samples/s",
-                    "h2d_bytes_per_step": int(cfg["nsamples"] * cfg["nchans"]),
-                    "d2h_bytes_per_step": int(d2h),
-                    "x_realtime": (cfg["nsamples"] * cfg["tsamp"]) / (el_e2e / 1e3 / e2e_steps)},
+            "config": config_block(cfg, plan.ntrials, len(task.chunks), world),
+            "x_realtime": (nsamples * cfg["tsamp"]) / (el / 1e3 / args.steps),
+            "e2e": {"value": e2e_value, "unit": "DM-trial*samples/s", "h2d_bytes_per_step": int(h2d_step),
+                    "d2h_bytes_per_step": int(d2h_step), "steps": e2e_steps,
+                    "x_realtime": (nsamples * cfg["tsamp"]) / (el_e2e / 1e3 / e2e_steps),
+                    "input_path": ("pinned host payload -> C ABI pgb_search_file_u8 (segmented H2D on a copy stream)"
+                                   if world == 1 else
+                                   "1/N rows per rank pinned H2D + peer pulls over NVLink (CUDA IPC)")},
             "roofline": {"bound": "alu", "kernel": "dedisp_u8_ring_persist_kernel<8,2,3,8>",
                          "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tadd/s",
                          "frac": achieved / peak, "traffic": load_ncu_traffic(),
+                         "smem_frac": achieved / smem_peak,
                          "per_unit": "nchans channel-adds per (trial, output sample)",
                          "launch_ms": per_launch_ms,
                          "note": "peak = measured CUDA-core 32-bit add rate (pgb_microbench_add_peak); "
-                                 "dedispersion moves ~2e-3 B per add, far right of the HBM ridge"},
+                                 "smem_frac = achieved / (128 B/clk/SM x 148 SMs x median SM clock) at one "
+                                 "shared-memory byte per add; dedispersion moves ~2e-3 HBM B per add"},
             "dedisp_share": (dd_ms / args.steps) / (el / args.steps),
             "gpu_launches": int(launches),
-            "clocks": clk.summary(),
+            "clocks": clocks,
         }
         if cpu:
             result["cpu_baseline"] = cpu
         print(json.dumps(result), flush=True)
+    if fan is not None:
+        fan.close()
     eng.close()
     if dist:
         dist.barrier()
@@ -394,19 +432,32 @@ def _native_add_peak(device: int) -> float:
     return v.value
 
 
+def _free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
 def main():
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--cpu-seconds", type=float, default=15.0,
-                    help="approximate CPU work of the cpu_baseline sample")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.warmup < 3:
         log("warmup raised to the contract minimum of 3")
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torch.distributed.run
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr=127.0.0.1", f"--master-port={_free_port()}", str(Path(__file__).resolve()),
+               *sys.argv[1:]]
+        log("launching: " + " ".join(cmd))
+        sys.exit(subprocess.call(cmd))
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
     local_rank = int(os.environ.get("LOCAL_RANK", 0))

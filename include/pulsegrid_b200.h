@@ -6,12 +6,12 @@
  * own; these entry points are what a maintainer binds to
  * replace, one for one:
  *
- *   pgb_generate_dm_trials  <- pulsegrid::generate_dm_trials   dedisp.hpp:117-118 (src/dedisp.cpp:28-70)
- *   pgb_delay_samples       <- pulsegrid::delay_samples        dedisp.hpp:112     (src/dedisp.cpp:13-18)
- *   pgb_adaptive_dm_step    <- pulsegrid::adaptive_dm_step     dedisp.hpp:115     (src/dedisp.cpp:20-26)
+ *   pgb_generate_dm_trials  <- pulsegrid::generate_dm_trials   dedisp.hpp:53-54   (src/dedisp.cpp:28-70)
+ *   pgb_delay_samples       <- pulsegrid::delay_samples        dedisp.hpp:48      (src/dedisp.cpp:13-18)
+ *   pgb_adaptive_dm_step    <- pulsegrid::adaptive_dm_step     dedisp.hpp:51      (src/dedisp.cpp:20-26)
  *   pgb_set_plan            <- the DmTrialPlan argument of run_dm_loop (dedisp.hpp:17-25), uploaded once
  *   pgb_run_dm_loop_u8/_f32 <- pulsegrid::run_dm_loop          engine.hpp:61-62   (src/engine.cpp:85-265)
- *   pgb_dedisperse_*        <- pulsegrid::dedisperse / dedisperse_block  dedisp.hpp:125-138
+ *   pgb_dedisperse_*        <- pulsegrid::dedisperse / dedisperse_block  dedisp.hpp:61,71-74 (src/dedisp.cpp:133-218)
  *   pgb_link_grid           <- pulsegrid::link_grid            cluster.hpp:43     (src/cluster.cpp:99-146)
  *   pgb_search_file_u8      <- pulsegrid::execute_task's chunk loop + sort + link_grid
  *                              (src/pipeline.cpp:72-106), fed raw 8-bit payload bytes
@@ -222,6 +222,39 @@ pgb_status pgb_fetch_file_candidates(pgb_context* ctx, pgb_candidate* out, size_
 /* (chunk index, trial) pairs, as FileOutcome::skipped_trials (pipeline.hpp:59). */
 pgb_status pgb_fetch_file_skipped(pgb_context* ctx, uint64_t* chunk_trial_pairs,
                                   size_t capacity, size_t* n_pairs);
+
+/* ---- bounded-memory streaming file search ------------------------------------ */
+/* execute_task with the prefetching reader (src/pipeline.cpp:66-106,
+ * src/filterbank.cpp:326-419): host and device memory stay at two chunks whatever the
+ * file size.  Protocol: pgb_stream_begin(plan of chunks); for k = 0..nchunks-1 in
+ * order: pgb_stream_buffer(k) -> read chunk k's [length][nchans] bytes into it ->
+ * pgb_stream_push(k, NULL) (or push a caller-owned host pointer); pgb_stream_finish
+ * sorts, clusters (radii == NULL: candidates only) and makes the results fetchable
+ * with the pgb_fetch_file_* / pgb_fetch_clusters calls.  The upload of chunk k runs
+ * on a copy stream while chunk k-1 computes; pgb_stream_buffer blocks only until the
+ * buffer's previous upload (chunk k-2) has left it, and may be called for chunk k+1
+ * from a reader thread while chunk k is being pushed. */
+pgb_status pgb_stream_begin(pgb_context* ctx, uint64_t nsamples, const pgb_chunk_spec* chunks,
+                            size_t nchunks, const pgb_engine_config* cfg,
+                            const pgb_link_radii* radii, const pgb_rfi_config* rfi);
+pgb_status pgb_stream_buffer(pgb_context* ctx, size_t chunk, uint8_t** host_buffer,
+                             size_t* capacity);
+pgb_status pgb_stream_push(pgb_context* ctx, size_t chunk, const uint8_t* bytes);
+pgb_status pgb_stream_finish(pgb_context* ctx, size_t* n_candidates, size_t* n_clusters);
+
+/* ---- multi-GPU payload fan-out ------------------------------------------------ */
+/* One process per GPU: each rank uploads 1/N of the file from host memory and pulls
+ * the other ranks' slices over NVLink from their device buffers (CUDA IPC), so the
+ * host link carries each byte once.  NCCL stays reserved for the candidate gather. */
+#define PGB_IPC_HANDLE_BYTES 64
+pgb_status pgb_device_alloc(int device, size_t bytes, void** device_ptr);
+pgb_status pgb_device_free(int device, void* device_ptr);
+pgb_status pgb_ipc_get_handle(const void* device_ptr, void* handle /* PGB_IPC_HANDLE_BYTES */);
+pgb_status pgb_ipc_open(int device, const void* handle, void** device_ptr);
+pgb_status pgb_ipc_close(void* device_ptr);
+/* Copy on the context's stream (any direction; peer device pointers included). */
+pgb_status pgb_copy_async(pgb_context* ctx, void* dst, const void* src, size_t bytes);
+pgb_status pgb_synchronize(pgb_context* ctx);
 
 /* ---- instrumentation --------------------------------------------------------- */
 /* Kernel launches issued by this context since creation (bench gpu_launches). */

@@ -332,6 +332,28 @@ class Reference(_Base):
         keys = ("wall", "read", "rfi", "dm_loop", "cluster", "write")
         return n.value, dict(zip(keys, ms.tolist()))
 
+    def search_file(self, path, **kw):
+        """execute_task's body on a file with structured results (parity mode by default).
+
+        Returns dict(candidates, clusters, members, skipped [k,2], cand_text, stage_ms)."""
+        f = self._fn("search_file", [_c.c_char_p, _c.POINTER(self.SearchParams), _c.POINTER(_vp),
+                                     _c.POINTER(_sz), _c.POINTER(_vp), _c.POINTER(_sz),
+                                     _c.POINTER(_vp), _c.POINTER(_vp), _c.POINTER(_sz),
+                                     _c.POINTER(_vp), _c.POINTER(_sz), _vp])
+        p = self._params(**kw)
+        pc, nc, pcl, ncl, pm, ps, ns, pt, nt = _vp(), _sz(), _vp(), _sz(), _vp(), _vp(), _sz(), _vp(), _sz()
+        ms = np.zeros(4, np.float64)
+        self._check(f(str(path).encode(), _c.byref(p), _c.byref(pc), _c.byref(nc), _c.byref(pcl),
+                      _c.byref(ncl), _c.byref(pm), _c.byref(ps), _c.byref(ns), _c.byref(pt),
+                      _c.byref(nt), abi.ptr(ms)))
+        cands = self._take(pc, nc.value, abi.CANDIDATE_DTYPE)
+        clusters = self._take(pcl, ncl.value, abi.CLUSTER_DTYPE)
+        members = self._take(pm, int(clusters["members"].sum()) if len(clusters) else 0, np.uint64)
+        skipped = self._take(ps, 2 * ns.value, np.uint64).reshape(-1, 2)
+        text = self._take(pt, nt.value, np.uint8).tobytes().decode()
+        return dict(candidates=cands, clusters=clusters, members=members, skipped=skipped,
+                    cand_text=text, stage_ms=dict(zip(("read", "rfi", "dm_loop", "cluster"), ms.tolist())))
+
     def create_task_plan(self, path, **kw):
         """(chunk specs, baseline_window) create_task resolves for a file."""
         f = self._fn("create_task_plan", [_c.c_char_p, _c.POINTER(self.SearchParams), _vp, _sz,

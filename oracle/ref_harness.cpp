@@ -11,6 +11,7 @@
 // (src/engine.cpp:95-97), which sidesteps the straggler-loop defect of
 // dedisperse_block (src/dedisp.cpp:188-195) and equals the
 // naive definition for every worker count.
+#include <algorithm>
 #include <chrono>
 #include <cstdlib>
 #include <cstring>
@@ -481,6 +482,88 @@ int pgref_execute_file(const char* path, const char* out_path, const pgref_searc
         }
         *n_clusters = outcome.candidates;
         return PGB_OK;
+    } catch (const std::exception& e) {
+        return fail(e);
+    }
+}
+
+// execute_task's body (src/pipeline.cpp:61-119) on a file, returning the structured
+// results instead of only the .cand text: the sorted file-level candidate list, the
+// link_grid clusters (+ flat member ids), the (chunk, trial) skipped pairs and the
+// .cand text.  Chunks are read synchronously (FilterbankReader::read_chunk; the
+// prefetching reader returns identical chunks) so memory stays at one chunk.
+int pgref_search_file(const char* path, const pgref_search_params* p, pgb_candidate** cands,
+                      size_t* ncands, pgb_cluster** clusters, size_t* nclusters,
+                      uint64_t** members, uint64_t** skipped /* pairs */, size_t* nskipped,
+                      char** cand_text, size_t* cand_len, double* stage_ms /*[4] read rfi loop cluster*/) {
+    try {
+        SearchParams params;
+        params.dm_lo = p->dm_lo;
+        params.dm_hi = p->dm_hi;
+        params.spacing = LinearSpacing{p->dm_step};
+        params.engine.n_workers = p->n_workers;
+        params.engine.detect_thresh = p->detect_thresh;
+        params.engine.boxcar_max = p->boxcar_max;
+        params.engine.radii = LinkRadii{p->radii.sep_time, p->radii.sep_dm_trials, p->radii.sep_width};
+        if (p->parity) params.engine.max_in_flight = p->n_workers;
+        params.baseline_len_s = p->baseline_len_s;
+        params.nsamps_chunk = p->nsamps_chunk;
+        params.rfi_narrowband = p->rfi_narrowband != 0;
+        params.rfi_broadband = p->rfi_broadband != 0;
+        params.k_sigma = p->k_sigma;
+        params.k_mad = p->k_mad;
+        auto task = create_task(path, params, "/dev/null");
+        BufferPool pool(task.engine.memory_budget);
+        FilterbankReader reader(path);
+        using clk = std::chrono::steady_clock;
+        auto ms = [](clk::time_point a) {
+            return std::chrono::duration<double, std::milli>(clk::now() - a).count();
+        };
+        double st[4] = {0, 0, 0, 0};
+        std::vector<Candidate> all;
+        std::vector<uint64_t> sk;
+        for (const auto& spec : task.chunks) {
+            auto t0 = clk::now();
+            Chunk chunk = reader.read_chunk(spec);
+            st[0] += ms(t0);
+            t0 = clk::now();
+            RfiMask mask;
+            mask.replacement = task.params.replacement;
+            if (task.params.rfi_narrowband) mask.bad_channels = flag_narrowband(chunk, task.params.k_mad);
+            if (task.params.rfi_broadband) mask.bad_samples = flag_broadband(chunk, task.params.k_sigma);
+            if (!mask.bad_channels.empty() || !mask.bad_samples.empty()) apply_mask(chunk, mask);
+            st[1] += ms(t0);
+            t0 = clk::now();
+            DmLoopResult r = run_dm_loop(chunk, task.plan, task.engine, pool);
+            st[2] += ms(t0);
+            all.insert(all.end(), r.candidates.begin(), r.candidates.end());
+            for (auto t : r.skipped_trials) {
+                sk.push_back(chunk.spec.index);
+                sk.push_back(t);
+            }
+        }
+        auto t0 = clk::now();
+        std::sort(all.begin(), all.end(), [](const Candidate& a, const Candidate& b) {
+            if (a.peak_sample != b.peak_sample) return a.peak_sample < b.peak_sample;
+            if (a.dm_trial != b.dm_trial) return a.dm_trial < b.dm_trial;
+            return a.width_index < b.width_index;
+        });
+        auto cl = link_grid(all, task.engine.radii);
+        st[3] = ms(t0);
+        if (stage_ms) std::memcpy(stage_ms, st, sizeof st);
+        std::vector<pgb_candidate> out(all.size());
+        if (!out.empty()) std::memcpy(out.data(), all.data(), out.size() * sizeof(Candidate));
+        *cands = dup(out);
+        *ncands = out.size();
+        *skipped = dup(sk);
+        *nskipped = sk.size() / 2;
+        std::ostringstream os;
+        write_candidates(cl, os);
+        const std::string s = os.str();
+        *cand_text = static_cast<char*>(std::malloc(s.size() + 1));
+        std::memcpy(*cand_text, s.c_str(), s.size() + 1);
+        *cand_len = s.size();
+        return export_clusters(cl, clusters, nclusters, members);
     } catch (const std::exception& e) {
         return fail(e);
     }

@@ -60,6 +60,18 @@ SIGNATURES = {
     "pgb_last_dedisp_time": ([_vp, _P(_c.c_double), _P(_u64), _P(_u64)], _int),
     "pgb_stream": ([_vp, _P(_vp)], _int),
     "pgb_microbench_add_peak": ([_int, _P(_c.c_double), _vp], _int),
+    "pgb_stream_begin": ([_vp, _u64, _vp, _sz, _P(abi.EngineConfigC), _P(abi.LinkRadiiC),
+                          _P(abi.RfiConfigC)], _int),
+    "pgb_stream_buffer": ([_vp, _sz, _P(_vp), _P(_sz)], _int),
+    "pgb_stream_push": ([_vp, _sz, _vp], _int),
+    "pgb_stream_finish": ([_vp, _P(_sz), _P(_sz)], _int),
+    "pgb_device_alloc": ([_int, _sz, _P(_vp)], _int),
+    "pgb_device_free": ([_int, _vp], _int),
+    "pgb_ipc_get_handle": ([_vp, _vp], _int),
+    "pgb_ipc_open": ([_int, _vp, _P(_vp)], _int),
+    "pgb_ipc_close": ([_vp], _int),
+    "pgb_copy_async": ([_vp, _vp, _vp, _sz], _int),
+    "pgb_synchronize": ([_vp], _int),
 }
 
 for _name, (_args, _res) in SIGNATURES.items():

@@ -12,6 +12,9 @@
 #include <mutex>
 #include <numeric>
 #include <stdexcept>
+#include <atomic>
+#include <thread>
+#include <vector>
 
 #include <chrono>
 #include <cstdio>
@@ -100,6 +103,8 @@ static size_t pool_aligned(size_t n) {
 
 using namespace pgb;
 
+struct ChunkRunHolder;
+
 struct pgb_context {
     int device = 0;
     cudaStream_t st = nullptr;
@@ -180,6 +185,29 @@ struct pgb_context {
     uint32_t last_nrows = 0;
     bool last_had_baseline = false;
     bool last_u8 = true;
+
+    // bounded-memory streaming file search (pgb_stream_*): two pinned host and two device
+    // chunk buffers, chunks pushed in order, synchronous back halves
+    struct Stream {
+        bool open = false;
+        uint64_t nsamples = 0;
+        std::vector<pgb_chunk_spec> chunks;
+        pgb_engine_config cfg{};
+        bool has_radii = false, has_rfi = false;
+        pgb_link_radii radii{};
+        pgb_rfi_config rfi{};
+        size_t next = 0;        // next chunk to push
+        uint64_t total = 0;     // candidates appended so far
+        uint64_t pitch_min = 0;
+        bool overlap = false, pending = false;
+        ChunkRunHolder* runs = nullptr;
+        PinnedBuf hbuf[2];
+        DevBuf dbuf[2];
+        cudaEvent_t up_done[2] = {}, dev_free[2] = {};
+        bool up_pending[2] = {false, false}, dev_pending[2] = {false, false};
+    } stream;
+    // host repack of widened 8-bit float chunks (pgb_run_dm_loop_f32 with host data)
+    PinnedBuf h_pack;
 };
 
 namespace {
@@ -325,6 +353,12 @@ struct ChunkRun {
     std::vector<uint32_t> active;
     std::vector<uint64_t> skipped;  // uncoverable trials (front) + degenerate ones (back)
 };
+
+}  // namespace
+struct ChunkRunHolder {
+    ChunkRun r[2];
+};
+namespace {
 
 void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spec,
                  const pgb_engine_config* cfg, int slot, ChunkRun& run) {
@@ -818,6 +852,61 @@ void chunk_back_async(pgb_context* ctx, ChunkRun& run, uint8_t* h_status, uint64
     ctx->launches += 12;
 }
 
+// Back half of a chunk with host reads (sync chunk_back): append its sorted candidates
+// to the file list and its skipped trials to the file's (chunk, trial) pairs.
+void append_chunk_sync(pgb_context* ctx, ChunkRun& run, uint64_t& total) {
+    chunk_back(ctx, run);
+    const uint64_t nc = ctx->n_cands;
+    if (nc) {
+        if ((total + nc) * sizeof(pgb_candidate) > ctx->file_cands.bytes) {
+            DevBuf grown;
+            grown.reserve(std::max<uint64_t>(2 * (total + nc), 4096) * sizeof(pgb_candidate));
+            if (total)
+                PGB_CUDA(cudaMemcpyAsync(grown.p, ctx->file_cands.p, total * sizeof(pgb_candidate),
+                                         cudaMemcpyDeviceToDevice, ctx->st));
+            PGB_CUDA(cudaStreamSynchronize(ctx->st));
+            ctx->file_cands.release();
+            ctx->file_cands = grown;
+            grown.p = nullptr;
+        }
+        PGB_CUDA(cudaMemcpyAsync(ctx->file_cands.as<pgb_candidate>() + total, ctx->cands_sorted.p,
+                                 nc * sizeof(pgb_candidate), cudaMemcpyDeviceToDevice, ctx->st));
+    }
+    total += nc;
+    for (uint64_t t : ctx->skipped) {
+        ctx->file_skipped.push_back(run.spec.index);
+        ctx->file_skipped.push_back(t);
+    }
+}
+
+// End of a file: the file-level sort (src/pipeline.cpp:100-105) and link_grid (:106).
+void file_sort_link(pgb_context* ctx, uint64_t total, const pgb_link_radii* radii,
+                    size_t* n_candidates, size_t* n_clusters) {
+    ctx->file_sorted.reserve(std::max<uint64_t>(total, 1) * sizeof(pgb_candidate));
+    if (total) {
+        const size_t tmp = sort_candidates_temp_bytes(total);
+        ctx->sort_tmp.reserve(tmp);
+        ctx->sort_keys.reserve(2 * total * sizeof(uint64_t));
+        ctx->sort_idx.reserve(2 * total * sizeof(uint32_t));
+        sort_candidates(ctx->file_cands.as<pgb_candidate>(), ctx->file_sorted.as<pgb_candidate>(), total,
+                        ctx->sort_tmp.p, tmp, ctx->sort_keys.as<uint64_t>(), ctx->sort_keys.as<uint64_t>() + total,
+                        ctx->sort_idx.as<uint32_t>(), ctx->sort_idx.as<uint32_t>() + total, ctx->st);
+    }
+    uint64_t ncl = 0;
+    if (radii)  // radii == NULL: candidates only (multi-GPU shards cluster after the gather)
+        cluster_candidates(ctx->file_sorted.as<pgb_candidate>(), total, *radii, ctx->cl_scratch, ctx->clusters,
+                           ctx->members, &ncl, ctx->st, &ctx->launches);
+    PGB_CUDA(cudaStreamSynchronize(ctx->st));
+    trace_mark(ctx, "file sort + link_grid", ctx->st);
+    trace_dump(ctx);
+    ctx->file_ncands = total;
+    ctx->n_clusters = ncl;
+    ctx->n_members = radii ? total : 0;
+    ctx->last_from_file = true;
+    if (n_candidates) *n_candidates = total;
+    if (n_clusters) *n_clusters = ncl;
+}
+
 // Runs the whole chain for one chunk whose samples are already on the device.
 void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spec,
                const pgb_engine_config* cfg) {
@@ -846,6 +935,34 @@ ChunkInput prepare_f32(pgb_context* ctx, const float* dptr, uint64_t length) {
     trace_mark(ctx, "integer check (pack)", ctx->st);
     if (*hflag == 0) return ChunkInput{ctx->in_u8.p, true};
     return ChunkInput{dptr, false};
+}
+
+// Parallel host repack of a float chunk into bytes; false if any cell is not an integer
+// in [0, 255] (then the caller uploads the floats and takes the fp32 path).
+bool host_pack_u8(const float* src, size_t n, uint8_t* dst) {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const size_t nt = std::min<size_t>(std::min<unsigned>(hw, 16u), std::max<size_t>(1, n >> 22));
+    std::atomic<bool> ok{true};
+    auto work = [&](size_t a, size_t b) {
+        constexpr size_t kBlk = 1 << 14;
+        for (size_t i = a; i < b && ok.load(std::memory_order_relaxed); i += kBlk) {
+            const size_t e = std::min(b, i + kBlk);
+            bool good = true;
+            for (size_t j = i; j < e; ++j) {
+                const float v = src[j];
+                const uint8_t q = (uint8_t)(int)v;
+                good &= (v >= 0.f) & (v <= 255.f) & ((float)q == v);
+                dst[j] = q;
+            }
+            if (!good) ok.store(false, std::memory_order_relaxed);
+        }
+    };
+    std::vector<std::thread> th;
+    const size_t per = (n + nt - 1) / nt;
+    for (size_t t = 1; t < nt; ++t) th.emplace_back(work, std::min(n, t * per), std::min(n, (t + 1) * per));
+    work(0, std::min(n, per));
+    for (auto& x : th) x.join();
+    return ok.load();
 }
 
 RfiParams to_rfi(const pgb_rfi_config* r) {
@@ -995,6 +1112,14 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         for (auto e : ctx->file_dd_ev) cudaEventDestroy(e);
         ctx->h_file_status.release();
         ctx->h_file_ctr.release();
+        ctx->h_pack.release();
+        for (int b = 0; b < 2; ++b) {
+            ctx->stream.hbuf[b].release();
+            ctx->stream.dbuf[b].release();
+            if (ctx->stream.up_done[b]) cudaEventDestroy(ctx->stream.up_done[b]);
+            if (ctx->stream.dev_free[b]) cudaEventDestroy(ctx->stream.dev_free[b]);
+        }
+        delete ctx->stream.runs;
         for (int k = 0; k < 2; ++k)
             for (cudaEvent_t e : {ctx->ev_dd0[k], ctx->ev_dd1[k], ctx->ev_front[k], ctx->ev_rms[k]})
                 cudaEventDestroy(e);
@@ -1062,14 +1187,24 @@ static pgb_status run_dm_loop_impl(pgb_context* ctx, const void* data, bool u8, 
         reset_timing(ctx);
         ctx->last_from_file = false;
         const void* dptr = data;
-        const size_t bytes = (size_t)spec->length * ctx->nchans * (u8 ? 1 : 4);
+        const size_t cells = (size_t)spec->length * ctx->nchans;
+        const size_t bytes = cells * (u8 ? 1 : 4);
+        bool as_u8 = u8;
         if (!on_device && ctx->ntrials) {
-            ctx->in_raw.reserve(bytes);
-            PGB_CUDA(cudaMemcpyAsync(ctx->in_raw.p, data, bytes, cudaMemcpyHostToDevice, ctx->st));
+            if (!u8) {
+                // read_chunk widens 8-bit files to floats (src/filterbank.cpp:304-307): repack
+                // integer chunks to bytes on the host threads, so a quarter of the bytes cross
+                // PCIe from pinned memory; any non-integer cell keeps the fp32 upload
+                ctx->h_pack.reserve(cells);
+                as_u8 = host_pack_u8(static_cast<const float*>(data), cells, ctx->h_pack.as<uint8_t>());
+            }
+            ctx->in_raw.reserve(as_u8 ? cells : bytes);
+            PGB_CUDA(cudaMemcpyAsync(ctx->in_raw.p, as_u8 && !u8 ? ctx->h_pack.p : data, as_u8 ? cells : bytes,
+                                     cudaMemcpyHostToDevice, ctx->st));
             dptr = ctx->in_raw.p;
         }
-        const ChunkInput ci = u8 ? ChunkInput{dptr, true}
-                                 : prepare_f32(ctx, static_cast<const float*>(dptr), spec->length);
+        const ChunkInput ci = as_u8 ? ChunkInput{dptr, true}
+                                    : prepare_f32(ctx, static_cast<const float*>(dptr), spec->length);
         run_chunk(ctx, ci, spec, cfg);
         if (n_candidates) *n_candidates = ctx->n_cands;
         if (n_skipped) *n_skipped = ctx->skipped.size();
@@ -1327,32 +1462,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
         ctx->trace = getenv("PGB_TRACE") != nullptr;
         trace_mark(ctx, "begin", ctx->st);
         uint64_t total = 0;
-        // back half of a chunk: append its sorted candidates and skipped trials
-        auto finish = [&](ChunkRun& run) {
-            chunk_back(ctx, run);
-            const uint64_t nc = ctx->n_cands;
-            if (nc) {
-                if ((total + nc) * sizeof(pgb_candidate) > ctx->file_cands.bytes) {
-                    DevBuf grown;
-                    grown.reserve(std::max<uint64_t>(2 * (total + nc), 4096) * sizeof(pgb_candidate));
-                    if (total)
-                        PGB_CUDA(cudaMemcpyAsync(grown.p, ctx->file_cands.p, total * sizeof(pgb_candidate),
-                                                 cudaMemcpyDeviceToDevice, ctx->st));
-                    PGB_CUDA(cudaStreamSynchronize(ctx->st));
-                    ctx->file_cands.release();
-                    ctx->file_cands = grown;
-                    grown.p = nullptr;
-                }
-                PGB_CUDA(cudaMemcpyAsync(ctx->file_cands.as<pgb_candidate>() + total,
-                                         ctx->cands_sorted.p, nc * sizeof(pgb_candidate),
-                                         cudaMemcpyDeviceToDevice, ctx->st));
-            }
-            total += nc;
-            for (uint64_t t : ctx->skipped) {
-                ctx->file_skipped.push_back(run.spec.index);
-                ctx->file_skipped.push_back(t);
-            }
-        };
+        auto finish = [&](ChunkRun& run) { append_chunk_sync(ctx, run, total); };
         // With a baseline the chain reads the slot's own baseline buffer, so chunk k's
         // front half (dedispersion + RMS) is issued before chunk k-1's back half: the
         // RMS of chunk k then runs beside the boxcar of chunk k-1.  Without one the
@@ -1482,31 +1592,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
             }
         }
         trace_mark(ctx, "chunks done (host sync)", ctx->st);
-        // file-level sort (src/pipeline.cpp:100-105) and link_grid (:106)
-        ctx->file_sorted.reserve(std::max<uint64_t>(total, 1) * sizeof(pgb_candidate));
-        if (total) {
-            const size_t tmp = sort_candidates_temp_bytes(total);
-            ctx->sort_tmp.reserve(tmp);
-            ctx->sort_keys.reserve(2 * total * sizeof(uint64_t));
-            ctx->sort_idx.reserve(2 * total * sizeof(uint32_t));
-            sort_candidates(ctx->file_cands.as<pgb_candidate>(), ctx->file_sorted.as<pgb_candidate>(),
-                            total, ctx->sort_tmp.p, tmp, ctx->sort_keys.as<uint64_t>(),
-                            ctx->sort_keys.as<uint64_t>() + total, ctx->sort_idx.as<uint32_t>(),
-                            ctx->sort_idx.as<uint32_t>() + total, ctx->st);
-        }
-        uint64_t ncl = 0;
-        if (radii)  // radii == NULL: candidates only (multi-GPU shards cluster after the gather)
-            cluster_candidates(ctx->file_sorted.as<pgb_candidate>(), total, *radii, ctx->cl_scratch,
-                               ctx->clusters, ctx->members, &ncl, ctx->st, &ctx->launches);
-        PGB_CUDA(cudaStreamSynchronize(ctx->st));
-        trace_mark(ctx, "file sort + link_grid", ctx->st);
-        trace_dump(ctx);
-        ctx->file_ncands = total;
-        ctx->n_clusters = ncl;
-        ctx->n_members = radii ? total : 0;
-        ctx->last_from_file = true;
-        if (n_candidates) *n_candidates = total;
-        if (n_clusters) *n_clusters = ncl;
+        file_sort_link(ctx, total, radii, n_candidates, n_clusters);
     });
 }
 
@@ -1552,6 +1638,216 @@ pgb_status pgb_stream(pgb_context* ctx, void** stream) {
     return guarded([&] {
         need(ctx && stream, PGB_ERR_ARGUMENT, "null argument");
         *stream = ctx->st;
+    });
+}
+
+// ---- bounded-memory streaming file search ---------------------------------------------
+// execute_task with the prefetching reader (src/pipeline.cpp:66-106,
+// src/filterbank.cpp:326-419): the caller reads chunk k into a pinned host buffer
+// (pgb_stream_buffer) and pushes it; the upload of chunk k runs on the copy stream
+// while chunk k-1 computes.  Host and device hold two chunks each, whatever the file
+// size.  Back halves are synchronous (per-chunk count reads), so a counter overflow
+// re-runs only that chunk's back half while its data is still resident.
+
+pgb_status pgb_stream_begin(pgb_context* ctx, uint64_t nsamples, const pgb_chunk_spec* chunks, size_t nchunks,
+                            const pgb_engine_config* cfg, const pgb_link_radii* radii,
+                            const pgb_rfi_config* rfi) {
+    return guarded([&] {
+        need(ctx && cfg && (nchunks == 0 || chunks), PGB_ERR_ARGUMENT, "null argument");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        auto& S = ctx->stream;
+        for (int b = 0; b < 2; ++b) {
+            if (!S.up_done[b]) PGB_CUDA(cudaEventCreateWithFlags(&S.up_done[b], cudaEventDisableTiming));
+            if (!S.dev_free[b]) PGB_CUDA(cudaEventCreateWithFlags(&S.dev_free[b], cudaEventDisableTiming));
+            if (S.up_pending[b]) PGB_CUDA(cudaEventSynchronize(S.up_done[b]));
+            S.up_pending[b] = S.dev_pending[b] = false;
+        }
+        for (size_t k = 0; k < nchunks; ++k) {
+            need(chunks[k].start_sample + chunks[k].length <= nsamples, PGB_ERR_INVALID_PLAN,
+                 "chunk extends past the file");
+            validate_cfg(ctx, &chunks[k], cfg);
+        }
+        if (!S.runs) S.runs = new ChunkRunHolder();
+        S.open = true;
+        S.nsamples = nsamples;
+        S.chunks.assign(chunks, chunks + nchunks);
+        S.cfg = *cfg;
+        S.has_radii = radii != nullptr;
+        if (radii) S.radii = *radii;
+        S.has_rfi = rfi && (rfi->narrowband || rfi->broadband);
+        if (S.has_rfi) S.rfi = *rfi;
+        S.next = 0;
+        S.total = 0;
+        S.pending = false;
+        S.overlap = cfg->baseline_window > 0;
+        S.pitch_min = 0;
+        uint64_t lmax = 0;
+        for (size_t k = 0; k < nchunks; ++k) {
+            S.pitch_min = std::max<uint64_t>(S.pitch_min, chunks[k].length);
+            lmax = std::max<uint64_t>(lmax, chunks[k].length);
+        }
+        const size_t cb = (size_t)lmax * ctx->nchans;
+        for (int b = 0; b < 2 && b < (int)nchunks; ++b) {
+            S.hbuf[b].reserve(cb);
+            S.dbuf[b].reserve(cb);
+        }
+        reset_timing(ctx);
+        ctx->file_skipped.clear();
+        ctx->ser_ok = false;
+        ctx->last_from_file = false;
+        ctx->trace = getenv("PGB_TRACE") != nullptr;
+        trace_mark(ctx, "stream begin", ctx->st);
+    });
+}
+
+pgb_status pgb_stream_buffer(pgb_context* ctx, size_t k, uint8_t** host_buffer, size_t* capacity) {
+    return guarded([&] {
+        need(ctx && host_buffer, PGB_ERR_ARGUMENT, "null argument");
+        auto& S = ctx->stream;
+        // the next chunk's buffer, or the one after it (a reader thread fills chunk k+1
+        // while chunk k is being pushed)
+        need(S.open && k >= S.next && k <= S.next + 1 && k < S.chunks.size(), PGB_ERR_ARGUMENT,
+             "stream buffer requested out of order (next or next + 1 only)");
+        const int b = (int)(k & 1);
+        if (S.up_pending[b]) {  // chunk k-2's upload still reads this host buffer
+            PGB_CUDA(cudaEventSynchronize(S.up_done[b]));
+            S.up_pending[b] = false;
+        }
+        *host_buffer = S.hbuf[b].as<uint8_t>();
+        if (capacity) *capacity = S.hbuf[b].bytes;
+    });
+}
+
+pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        auto& S = ctx->stream;
+        need(S.open && k == S.next && k < S.chunks.size(), PGB_ERR_ARGUMENT, "chunks are pushed in order");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        // every earlier push ended with a stream sync (append_chunk_sync), so the pinned
+        // staging arena of the small per-chunk uploads is free again
+        if (k > 0) stage_reset(ctx);
+        const pgb_chunk_spec& spec = S.chunks[k];
+        const uint32_t C = ctx->nchans;
+        const int b = (int)(k & 1);
+        const size_t cb = (size_t)spec.length * C;
+        // the device buffer held chunk k-2 until its front half (transpose / RFI) read it
+        if (S.dev_pending[b]) PGB_CUDA(cudaStreamWaitEvent(ctx->copy_st, S.dev_free[b], 0));
+        if (bytes && bytes != S.hbuf[b].as<uint8_t>() && S.up_pending[b]) {
+            PGB_CUDA(cudaEventSynchronize(S.up_done[b]));
+            S.up_pending[b] = false;
+        }
+        PGB_CUDA(cudaMemcpyAsync(S.dbuf[b].p, bytes ? bytes : S.hbuf[b].as<uint8_t>(), cb,
+                                 cudaMemcpyHostToDevice, ctx->copy_st));
+        PGB_CUDA(cudaEventRecord(S.up_done[b], ctx->copy_st));
+        S.up_pending[b] = true;
+        PGB_CUDA(cudaStreamWaitEvent(ctx->st, S.up_done[b], 0));
+        trace_mark(ctx, "chunk upload waited", ctx->st);
+        const uint8_t* cptr = S.dbuf[b].as<uint8_t>();
+        ChunkInput ci{cptr, true};
+        ci.raw = true;
+        ci.pitch_min = S.pitch_min;
+        ci.more = S.overlap && k + 1 < S.chunks.size();
+        if (S.has_rfi) {  // src/pipeline.cpp:79-87
+            uint64_t nbc = 0, nbs = 0;
+            ctx->rfi_out.reserve(cb * 4);
+            rfi_clean_impl<uint8_t>(cptr, spec.length, C, to_rfi(&S.rfi), ctx->rfi, ctx->rfi_out.as<float>(), ctx->st,
+                                    &nbc, &nbs);
+            ctx->launches += 8;
+            if (nbc || nbs) {
+                ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), spec.length);
+                ci.pitch_min = S.pitch_min;
+                ci.more = S.overlap && k + 1 < S.chunks.size();
+            }
+        }
+        ChunkRun* runs = S.runs->r;
+        ChunkRun& cur = runs[k & 1];
+        chunk_front(ctx, ci, &spec, &S.cfg, (int)(k & 1), cur);
+        PGB_CUDA(cudaEventRecord(S.dev_free[b], ctx->st));
+        S.dev_pending[b] = true;
+        if (S.pending) append_chunk_sync(ctx, runs[(k - 1) & 1], S.total);
+        S.pending = true;
+        if (!S.overlap) {
+            append_chunk_sync(ctx, cur, S.total);
+            S.pending = false;
+        }
+        ++S.next;
+    });
+}
+
+pgb_status pgb_stream_finish(pgb_context* ctx, size_t* n_candidates, size_t* n_clusters) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        auto& S = ctx->stream;
+        need(S.open && S.next == S.chunks.size(), PGB_ERR_ARGUMENT, "not every chunk was pushed");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        if (S.pending) append_chunk_sync(ctx, S.runs->r[(S.next - 1) & 1], S.total);
+        S.pending = false;
+        S.open = false;
+        trace_mark(ctx, "chunks done (host sync)", ctx->st);
+        file_sort_link(ctx, S.total, S.has_radii ? &S.radii : nullptr, n_candidates, n_clusters);
+        for (int b = 0; b < 2; ++b) S.up_pending[b] = S.dev_pending[b] = false;  // stream synced
+    });
+}
+
+// ---- multi-GPU payload fan-out (CUDA IPC over NVLink) -----------------------------------
+// A dedicated cudaMalloc allocation, so its IPC handle maps exactly this buffer (a
+// sub-allocation of a caching allocator would export its whole segment).
+pgb_status pgb_device_alloc(int device, size_t bytes, void** device_ptr) {
+    return guarded([&] {
+        need(device_ptr && bytes, PGB_ERR_ARGUMENT, "null argument");
+        PGB_CUDA(cudaSetDevice(device));
+        if (cudaMalloc(device_ptr, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            raise(PGB_ERR_OOM, "device allocation of " + std::to_string(bytes) + " bytes failed");
+        }
+    });
+}
+
+pgb_status pgb_device_free(int device, void* device_ptr) {
+    return guarded([&] {
+        PGB_CUDA(cudaSetDevice(device));
+        PGB_CUDA(cudaFree(device_ptr));
+    });
+}
+
+pgb_status pgb_ipc_get_handle(const void* device_ptr, void* handle) {
+    return guarded([&] {
+        need(device_ptr && handle, PGB_ERR_ARGUMENT, "null argument");
+        static_assert(sizeof(cudaIpcMemHandle_t) == PGB_IPC_HANDLE_BYTES, "IPC handle size");
+        cudaIpcMemHandle_t h;
+        PGB_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(device_ptr)));
+        std::memcpy(handle, &h, sizeof h);
+    });
+}
+
+pgb_status pgb_ipc_open(int device, const void* handle, void** device_ptr) {
+    return guarded([&] {
+        need(handle && device_ptr, PGB_ERR_ARGUMENT, "null argument");
+        PGB_CUDA(cudaSetDevice(device));
+        cudaIpcMemHandle_t h;
+        std::memcpy(&h, handle, sizeof h);
+        PGB_CUDA(cudaIpcOpenMemHandle(device_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    });
+}
+
+pgb_status pgb_ipc_close(void* device_ptr) {
+    return guarded([&] { PGB_CUDA(cudaIpcCloseMemHandle(device_ptr)); });
+}
+
+pgb_status pgb_copy_async(pgb_context* ctx, void* dst, const void* src, size_t bytes) {
+    return guarded([&] {
+        need(ctx && (bytes == 0 || (dst && src)), PGB_ERR_ARGUMENT, "null argument");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        if (bytes) PGB_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, ctx->st));
+    });
+}
+
+pgb_status pgb_synchronize(pgb_context* ctx) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        PGB_CUDA(cudaStreamSynchronize(ctx->st));
     });
 }
 

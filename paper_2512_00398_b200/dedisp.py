@@ -1,6 +1,6 @@
 """DM-trial plan: pulsegrid's dedisp.hpp host API (delay model and trial grid).
 
-Mirrors /root/reference/proj/include/pulsegrid/dedisp.hpp:13-120 and
+Mirrors /root/reference/proj/include/pulsegrid/dedisp.hpp:13-76 and
 src/dedisp.cpp:13-74.  The arithmetic runs in libpgb200 (C++ compiled with the
 reference build's FMA contractions spelled out), so delays are bit-identical to
 the reference library's.

@@ -11,9 +11,12 @@ produces -- and runs link_grid, so the output is identical for any world size.
 """
 from __future__ import annotations
 
+import ctypes
+
 import numpy as np
 
 from . import abi
+from ._native import check, lib
 
 
 def trial_work(plan, chunk_lengths) -> np.ndarray:
@@ -64,15 +67,17 @@ def sort_candidates(c: np.ndarray) -> np.ndarray:
     return c[order]
 
 
-def gather_candidates(local: np.ndarray, *, device=None, group=None) -> np.ndarray | None:
-    """All ranks contribute their candidate records; rank 0 gets the merged, sorted list
-    (other ranks get None).  Records travel as raw bytes in one padded all_gather."""
+def gather_records(local: np.ndarray, *, device=None, group=None) -> np.ndarray | None:
+    """Concatenate every rank's fixed-width records on rank 0 (other ranks get None).
+    Counts travel in one all_gather, then the raw bytes padded to the largest count in a
+    second (NCCL over NVLink for CUDA devices, gloo on CPU)."""
     import torch
     import torch.distributed as dist
 
     world = dist.get_world_size(group)
     rank = dist.get_rank(group)
-    itemsize = abi.CANDIDATE_DTYPE.itemsize
+    local = np.ascontiguousarray(local)
+    itemsize = local.dtype.itemsize
     dev = device if device is not None else torch.device("cpu")
     n = torch.tensor([len(local)], dtype=torch.int64, device=dev)
     counts = [torch.zeros_like(n) for _ in range(world)]
@@ -81,26 +86,117 @@ def gather_candidates(local: np.ndarray, *, device=None, group=None) -> np.ndarr
     cap = max(1, max(counts))
     buf = torch.zeros(cap * itemsize, dtype=torch.uint8, device=dev)
     if len(local):
-        raw = torch.from_numpy(np.ascontiguousarray(local).view(np.uint8).copy())
+        raw = torch.from_numpy(local.view(np.uint8).reshape(-1).copy())
         buf[: raw.numel()] = raw.to(dev)
     bufs = [torch.zeros_like(buf) for _ in range(world)]
     dist.all_gather(bufs, buf, group=group)
     if rank != 0:
         return None
     # (np.concatenate would canonicalise the padded 72-byte record dtype)
-    merged = np.zeros(sum(counts), abi.CANDIDATE_DTYPE)
-    raw = merged.view(np.uint8)
+    merged = np.zeros(sum(counts), local.dtype)
+    raw = merged.view(np.uint8).reshape(-1)
     off = 0
     for r, b in enumerate(bufs):
         if counts[r]:
             nb = counts[r] * itemsize
             raw[off: off + nb] = b[:nb].cpu().numpy()
             off += nb
-    return sort_candidates(merged)
+    return merged
 
 
-def search_file_distributed(payload, task, *, rank: int, world: int, device: int, group=None):
-    """Sharded file search; rank 0 returns the SearchResult, other ranks None."""
+def gather_candidates(local: np.ndarray, *, device=None, group=None) -> np.ndarray | None:
+    """All ranks contribute their candidate records; rank 0 gets the merged list sorted
+    by (peak_sample, dm_trial, width_index) -- the single-device order."""
+    merged = gather_records(np.ascontiguousarray(local, abi.CANDIDATE_DTYPE), device=device, group=group)
+    return None if merged is None else sort_candidates(merged)
+
+
+def gather_skipped(pairs: np.ndarray, *, device=None, group=None) -> np.ndarray | None:
+    """(chunk, trial) skipped pairs of every shard, merged on rank 0 and sorted by
+    (chunk, trial) -- FileOutcome::skipped_trials order (src/pipeline.cpp:95-96)."""
+    pairs = np.ascontiguousarray(np.asarray(pairs, np.uint64).reshape(-1, 2))
+    rec = pairs.view(np.dtype([("chunk", "<u8"), ("trial", "<u8")])).reshape(-1)
+    merged = gather_records(rec, device=device, group=group)
+    if merged is None:
+        return None
+    merged = np.sort(merged, order=("chunk", "trial"))
+    return merged.view(np.uint64).reshape(-1, 2)
+
+
+def row_slices(nsamples: int, world: int) -> list[tuple[int, int]]:
+    """Rows of the file each rank uploads from host memory (equal contiguous slices)."""
+    return [(nsamples * r // world, nsamples * (r + 1) // world) for r in range(world)]
+
+
+class PayloadFanout:
+    """Multi-GPU input path: every rank uploads 1/N of the file's rows from host memory
+    into its own device buffer, then pulls the other ranks' rows over NVLink from their
+    buffers (CUDA IPC, cudaMemcpyAsync between peers).  The host link carries each byte
+    once per node instead of once per GPU; NCCL stays reserved for the candidate gather.
+    """
+
+    def __init__(self, eng, nsamples: int, nchans: int, *, group=None):
+        import torch.distributed as dist
+
+        from .engine import DeviceBuffer
+
+        self.eng = eng
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.nchans = nchans
+        self.buf = DeviceBuffer(eng.device, (nsamples, nchans))
+        handles = [None] * self.world
+        dist.all_gather_object(handles, self.buf.ipc_handle(), group=group)
+        self.peers: dict[int, int] = {}
+        for r, h in enumerate(handles):
+            if r != self.rank:
+                p = ctypes.c_void_p()
+                check(lib.pgb_ipc_open(eng.device, (ctypes.c_uint8 * 64).from_buffer_copy(h), ctypes.byref(p)))
+                self.peers[r] = int(p.value)
+        self.slices = row_slices(nsamples, self.world)
+
+    @property
+    def own_rows(self) -> tuple[int, int]:
+        return self.slices[self.rank]
+
+    def upload_own(self, host_rows: np.ndarray) -> int:
+        """H2D of this rank's rows (host_rows = rows own_rows[0]:own_rows[1], ideally pinned)."""
+        r0, r1 = self.own_rows
+        nb = (r1 - r0) * self.nchans
+        assert host_rows.nbytes == nb and host_rows.flags.c_contiguous
+        self.eng.copy_async(self.buf.ptr + r0 * self.nchans, host_rows.ctypes.data, nb)
+        return nb
+
+    def exchange(self) -> int:
+        """Wait until every rank's rows are resident, then pull the peers' rows (bytes pulled)."""
+        import torch.distributed as dist
+
+        self.eng.synchronize()
+        dist.barrier(group=self.group)
+        pulled = 0
+        for r, ptr in self.peers.items():
+            a, b = self.slices[r]
+            nb = (b - a) * self.nchans
+            self.eng.copy_async(self.buf.ptr + a * self.nchans, ptr + a * self.nchans, nb)
+            pulled += nb
+        return pulled
+
+    def close(self) -> None:
+        import torch.distributed as dist
+
+        self.eng.synchronize()
+        dist.barrier(group=self.group)  # no peer still reads our buffer
+        for ptr in self.peers.values():
+            check(lib.pgb_ipc_close(ctypes.c_void_p(ptr)))
+        self.peers.clear()
+        self.buf.free()
+
+
+def search_file_distributed(payload, task, *, rank: int, world: int, device: int, group=None,
+                            gather_device=None):
+    """Sharded file search; rank 0 returns the SearchResult (candidates, clusters and the
+    skipped pairs of every shard), other ranks None."""
     import torch
 
     from .engine import default_engine
@@ -110,9 +206,11 @@ def search_file_distributed(payload, task, *, rank: int, world: int, device: int
     lo, hi = shard_trials(work, world, DD_TRIAL_BLOCK)[rank]
     eng = default_engine(device)
     cands, _, skipped = eng.search_file(payload, task.header.nsamples, task.chunks, task.plan,
-                                        task.engine, trial_range=(lo, hi), cluster=False)
-    merged = gather_candidates(cands, device=torch.device("cuda", device), group=group)
+                                        task.engine, trial_range=(lo, hi), cluster=False, rfi=task.rfi)
+    gdev = gather_device if gather_device is not None else torch.device("cuda", device)
+    merged = gather_candidates(cands, device=gdev, group=group)
+    all_skipped = gather_skipped(skipped, device=gdev, group=group)
     if rank != 0:
         return None
     clusters = eng.link_grid(merged, task.engine.radii)
-    return SearchResult(merged, clusters, skipped)
+    return SearchResult(merged, clusters, all_skipped)

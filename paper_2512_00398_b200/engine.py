@@ -171,8 +171,35 @@ def in_flight_limit(plan: DmTrialPlan, chunk_len: int, cfg: EngineConfig) -> int
     return limit
 
 
+class DeviceBuffer:
+    """A dedicated device allocation (pgb_device_alloc) holding a [rows][nchans] u8 payload.
+
+    Usable as a `search_file` payload like a CUDA tensor, and exportable to the other
+    ranks of a node over CUDA IPC (its handle maps exactly this buffer)."""
+
+    def __init__(self, device: int, shape: tuple[int, int]):
+        self.device = int(device)
+        self.shape = (int(shape[0]), int(shape[1]))
+        self.nbytes = self.shape[0] * self.shape[1]
+        p = ctypes.c_void_p()
+        check(lib.pgb_device_alloc(self.device, self.nbytes, ctypes.byref(p)))
+        self.ptr = int(p.value)
+
+    def ipc_handle(self) -> bytes:
+        h = (ctypes.c_uint8 * 64)()
+        check(lib.pgb_ipc_get_handle(ctypes.c_void_p(self.ptr), h))
+        return bytes(h)
+
+    def free(self) -> None:
+        if self.ptr:
+            check(lib.pgb_device_free(self.device, ctypes.c_void_p(self.ptr)))
+            self.ptr = 0
+
+
 def _device_tensor(x):
-    """(data_ptr, is_u8, device) for a CUDA torch tensor, else None."""
+    """(data_ptr, is_u8, device) for a CUDA torch tensor or a DeviceBuffer, else None."""
+    if isinstance(x, DeviceBuffer):
+        return x.ptr, True, x.device
     try:
         import torch
     except ImportError:  # pragma: no cover
@@ -341,9 +368,10 @@ class Engine:
         nc, ncl = ctypes.c_size_t(), ctypes.c_size_t()
         dev = _device_tensor(payload)
         if dev is not None:
-            import torch
+            if not isinstance(payload, DeviceBuffer):
+                import torch
 
-            torch.cuda.current_stream().synchronize()
+                torch.cuda.current_stream().synchronize()
             ptr, on_dev = ctypes.c_void_p(dev[0]), 1
         else:
             payload = np.ascontiguousarray(payload, dtype=np.uint8)
@@ -356,6 +384,71 @@ class Engine:
                                      ctypes.byref(ccfg), rp, ctypes.byref(rc) if rc is not None else None,
                                      ctypes.byref(nc), ctypes.byref(ncl)))
         return self.fetch_file_results(nc.value, ncl.value)
+
+    def search_stream(self, fd: int, data_offset: int, nsamples: int, chunks: list[ChunkSpec],
+                      plan: DmTrialPlan, cfg: EngineConfig, *, trial_range: tuple[int, int] | None = None,
+                      cluster: bool = True, rfi: RfiConfig | None = None, read_threads: int = 4):
+        """execute_task with the prefetching reader on an open 8-bit filterbank (bounded memory).
+
+        Chunk k is read from `fd` (payload at `data_offset`, [nsamples][nchans] bytes) by
+        `read_threads` parallel preads straight into the context's pinned buffer while
+        chunk k-1 is pushed; host and device memory stay at two chunks
+        (src/pipeline.cpp:66-106, src/filterbank.cpp:326-419)."""
+        import os
+        from concurrent.futures import ThreadPoolExecutor
+
+        self.set_plan(plan, trial_range)
+        arr = np.zeros(len(chunks), abi.CHUNK_SPEC_DTYPE)
+        for k, c in enumerate(chunks):
+            arr[k] = (c.index, c.start_sample, c.length, c.overlap, c.valid_begin, c.valid_end)
+        ccfg = cfg._c()
+        r = cfg.radii._c()
+        rc = rfi._c() if (rfi is not None and rfi.active) else None
+        check(lib.pgb_stream_begin(self._h, int(nsamples), abi.ptr(arr), len(arr), ctypes.byref(ccfg),
+                                   ctypes.byref(r) if cluster else None,
+                                   ctypes.byref(rc) if rc is not None else None))
+        C = plan.nchans
+        pool = ThreadPoolExecutor(max(1, read_threads))
+
+        def fill(k: int) -> None:
+            p, cap = ctypes.c_void_p(), ctypes.c_size_t()
+            check(lib.pgb_stream_buffer(self._h, k, ctypes.byref(p), ctypes.byref(cap)))
+            nbytes = chunks[k].length * C
+            buf = (ctypes.c_uint8 * nbytes).from_address(p.value)
+            mv = memoryview(buf).cast("B")
+            off0 = data_offset + chunks[k].start_sample * C
+            step = -(-nbytes // max(1, read_threads))
+
+            def rd(a: int) -> None:
+                b = min(nbytes, a + step)
+                while a < b:
+                    n = os.preadv(fd, [mv[a:b]], off0 + a)
+                    if n <= 0:
+                        raise OSError(f"short read at byte {off0 + a}")
+                    a += n
+
+            list(pool.map(rd, range(0, nbytes, step)))
+
+        try:
+            with ThreadPoolExecutor(1) as reader:
+                fut = reader.submit(fill, 0) if chunks else None
+                for k in range(len(chunks)):
+                    fut.result()
+                    if k + 1 < len(chunks):
+                        fut = reader.submit(fill, k + 1)
+                    check(lib.pgb_stream_push(self._h, k, None))
+        finally:
+            pool.shutdown()
+        nc, ncl = ctypes.c_size_t(), ctypes.c_size_t()
+        check(lib.pgb_stream_finish(self._h, ctypes.byref(nc), ctypes.byref(ncl)))
+        return self.fetch_file_results(nc.value, ncl.value)
+
+    def copy_async(self, dst: int, src: int, nbytes: int) -> None:
+        """cudaMemcpyAsync on this context's stream (host, device or peer pointers)."""
+        check(lib.pgb_copy_async(self._h, ctypes.c_void_p(dst), ctypes.c_void_p(src), int(nbytes)))
+
+    def synchronize(self) -> None:
+        check(lib.pgb_synchronize(self._h))
 
     # ---- RFI excision --------------------------------------------------------------------
     def rfi_clean(self, chunk_data: np.ndarray, plan: DmTrialPlan, rfi: RfiConfig):

@@ -168,11 +168,15 @@ _DBL_KEYS = {"fch1", "foff", "tsamp", "tstart", "az_start", "za_start", "src_raj
 _STR_KEYS = {"source_name", "rawdatafile"}
 
 
-def read_filterbank(path: str | Path) -> tuple[FilterbankHeader, np.ndarray]:
-    """Header + the raw 8-bit payload as [nsamples][nchans] (no float widening)."""
+def read_filterbank_header(path: str | Path) -> tuple[FilterbankHeader, int]:
+    """SIGPROC header (src/filterbank.cpp:102-175) and the payload's byte offset; nsamples
+    is derived from the file size like the reference (payload / bytes per sample)."""
     from .errors import PulsegridError
 
-    raw = Path(path).read_bytes()
+    path = Path(path)
+    with open(path, "rb") as f:
+        raw = f.read(1 << 16)
+    size = path.stat().st_size
     pos = 0
 
     def rstr():
@@ -206,12 +210,39 @@ def read_filterbank(path: str | Path) -> tuple[FilterbankHeader, np.ndarray]:
     nchans, nbits = int(vals.get("nchans", 0)), int(vals.get("nbits", 0))
     if nbits != 8:
         raise PulsegridError(f"raw ingest needs nbits=8 (file has {nbits})")
-    payload = np.frombuffer(raw, dtype=np.uint8, offset=pos)
-    if payload.size % nchans:
+    payload = size - pos
+    if nchans <= 0 or payload % nchans:
         raise PulsegridError("payload is not a whole number of samples")
     hdr = FilterbankHeader(fch1=float(vals["fch1"]), foff=float(vals["foff"]), nchans=nchans,
-                           tsamp=float(vals["tsamp"]), nbits=nbits,
-                           nsamples=payload.size // nchans,
+                           tsamp=float(vals["tsamp"]), nbits=nbits, nsamples=payload // nchans,
                            source_name=str(vals.get("source_name", "")),
                            tstart=float(vals.get("tstart", 0.0)))
-    return hdr, payload.reshape(-1, nchans)
+    return hdr, pos
+
+
+def read_filterbank(path: str | Path) -> tuple[FilterbankHeader, np.ndarray]:
+    """Header + the raw 8-bit payload as [nsamples][nchans] (no float widening; whole file
+    in memory -- `search_fil` streams instead)."""
+    hdr, off = read_filterbank_header(path)
+    payload = np.fromfile(path, dtype=np.uint8, offset=off)
+    return hdr, payload.reshape(-1, hdr.nchans)
+
+
+def search_fil(path: str | Path, params: SearchParams, *, device: int = 0, read_threads: int = 4,
+               trial_range: tuple[int, int] | None = None) -> SearchResult:
+    """create_task + execute_task on an 8-bit SIGPROC file with bounded memory
+    (src/pipeline.cpp:32-119): chunks are read straight into pinned buffers by parallel
+    preads while the previous chunk computes; host and device hold two chunks."""
+    import os
+
+    hdr, off = read_filterbank_header(path)
+    task = create_task(hdr, params)
+    eng = default_engine(device)
+    fd = os.open(str(path), os.O_RDONLY)
+    try:
+        cands, clusters, skipped = eng.search_stream(fd, off, hdr.nsamples, task.chunks, task.plan,
+                                                     task.engine, trial_range=trial_range, rfi=task.rfi,
+                                                     read_threads=read_threads)
+    finally:
+        os.close(fd)
+    return SearchResult(cands, clusters, skipped)

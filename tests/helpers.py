@@ -77,3 +77,20 @@ def clusters_equal(got, want_recs: np.ndarray, want_members: np.ndarray):
         a = got.member_ids(i)
         off, cnt = int(wr["member_offset"][i]), int(wr["members"][i])
         assert np.array_equal(a, want_members[off: off + cnt]), i
+
+
+def task_for(cfg: dict):
+    """The product's create_task for a tools/synth.py config dict (reference defaults
+    otherwise: one worker, link radii 3/9/3; RFI on exactly when the config says so)."""
+    from paper_2512_00398_b200.engine import EngineConfig, RfiConfig
+    from paper_2512_00398_b200.pipeline import SearchParams, create_task
+
+    hdr = FilterbankHeader(fch1=cfg["fch1"], foff=cfg["foff"], nchans=cfg["nchans"],
+                           tsamp=cfg["tsamp"], nsamples=cfg["nsamples"])
+    rfi = bool(cfg.get("rfi", False))
+    params = SearchParams(dm_lo=cfg["dm_lo"], dm_hi=cfg["dm_hi"], spacing=LinearSpacing(cfg["dm_step"]),
+                          engine=EngineConfig(n_workers=1, detect_thresh=cfg["detect_thresh"],
+                                              boxcar_max=cfg["boxcar_max"]),
+                          baseline_len_s=cfg["baseline_s"], nsamps_chunk=cfg["nsamps_chunk"],
+                          rfi=RfiConfig(narrowband=rfi, broadband=rfi))
+    return create_task(hdr, params)

@@ -100,3 +100,37 @@ def test_shard_trials_block_granule():
         cost = [32 * sum(w[b:b + 32].max() for b in range(lo, hi, 32)) for lo, hi in shards]
         assert max(cost) - min(cost) <= 2 * 32 * w.max()
     assert shard_trials(w[:40], 4, 32) == shard_trials(w[:40], 4)  # too few blocks: plain split
+
+
+def _skip_worker(rank, world, port, out_q):
+    import torch.distributed as dist
+
+    from paper_2512_00398_b200.distributed import gather_skipped
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    # shard r skipped trials r, r+2, ... of chunks 0 and 3 (listed chunk-major per shard)
+    mine = np.array([(c, t) for c in (0, 3) for t in range(rank, 12, world)], np.uint64)
+    merged = gather_skipped(mine if rank else mine[:0].reshape(0, 2))  # rank 0 skipped none
+    if rank == 0:
+        out_q.put(merged.tobytes())
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_gather_skipped_pairs_sorted_by_chunk_then_trial():
+    """the (chunk, trial) skipped pairs of every shard reach rank 0, ordered like
+    FileOutcome::skipped_trials (chunk by chunk, trials ascending)."""
+    world = 3
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_skip_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = np.frombuffer(q.get(timeout=120), np.uint64).reshape(-1, 2)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    want = np.array(sorted((c, t) for c in (0, 3) for t in range(12) if t % world != 0), np.uint64)
+    assert np.array_equal(got, want)

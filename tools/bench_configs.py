@@ -23,35 +23,15 @@ import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import bench  # noqa: E402
+from tools import synth  # noqa: E402
 from paper_2512_00398_b200.engine import default_engine  # noqa: E402
 
-CONFIGS = {
-    "A": dict(workload="config_A", nchans=1024, fch1=1500.0, foff=-0.25, tsamp=64e-6, nsamples=1 << 16,
-              dm_lo=0.0, dm_hi=500.0, dm_step=2.0, boxcar_max=4096, detect_thresh=6.0, baseline_s=2.0,
-              nsamps_chunk=1 << 18, npulses=3, seed=1000),
-    "C": dict(workload="config_C_fast_like", nchans=4096, fch1=1500.0, foff=-0.1220703125, tsamp=49.152e-6,
-              nsamples=1 << 22, dm_lo=0.0, dm_hi=5000.0, dm_step=1.25, boxcar_max=4096, detect_thresh=6.0,
-              baseline_s=2.0, nsamps_chunk=1 << 20, npulses=8, seed=3000),
-    "E": dict(workload="config_E_rfi_stress", nchans=8192, fch1=1500.0, foff=-0.0625, tsamp=64e-6,
-              nsamples=1 << 20, dm_lo=0.0, dm_hi=2047.5, dm_step=0.5, boxcar_max=4096, detect_thresh=6.0,
-              baseline_s=2.0, nsamps_chunk=1 << 19, npulses=50, seed=5000, rfi=True),
-}
-
-
-def add_rfi(payload: torch.Tensor, cfg, rng):
-    """Dense RFI for config E: 5% hot channels and DM-0 bursts every ~4096 samples."""
-    n, nch = payload.shape
-    hot = torch.from_numpy(rng.choice(nch, nch // 20, replace=False)).to(payload.device)
-    payload[:, hot] = torch.clamp(payload[:, hot].to(torch.int16) + 40, 0, 255).to(torch.uint8)
-    for t in range(2048, n - 2, 4096):
-        payload[t: t + 2] = torch.clamp(payload[t: t + 2].to(torch.int16) + 30, 0, 255).to(torch.uint8)
+CONFIGS = {k: v for k, v in synth.CONFIGS.items() if k in ("A", "C", "E")}
 
 
 def run_file(cfg, steps, label=None):
     task = bench.build_task(cfg)
     payload = bench.make_payload(cfg, task.plan)
-    if cfg.get("rfi"):
-        add_rfi(payload, cfg, np.random.default_rng(cfg["seed"]))
     torch.cuda.synchronize()
     eng = default_engine(0)
     eng.search_file(payload, cfg["nsamples"], task.chunks, task.plan, task.engine, rfi=task.rfi)  # warm-up
