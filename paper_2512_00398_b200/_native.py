@@ -74,16 +74,36 @@ SIGNATURES = {
     "pgb_synchronize": ([_vp], _int),
 }
 
-for _name, (_args, _res) in SIGNATURES.items():
-    _f = getattr(lib, _name)
-    _f.argtypes = _args
-    _f.restype = _res
+def _bind(handle: ctypes.CDLL) -> ctypes.CDLL:
+    for name, (args, res) in SIGNATURES.items():
+        f = getattr(handle, name)
+        f.argtypes = args
+        f.restype = res
+    return handle
 
 
-def check(rc: int) -> None:
-    """Raise the pulsegrid exception named by a pgb_status."""
+_bind(lib)
+
+ABLATION_LIB_PATH = LIB_PATH.with_name("libpgb200_ablations.so")
+_ablation = None
+
+
+def ablation_lib() -> ctypes.CDLL:
+    """libpgb200_ablations.so (csrc/Makefile, -DPGB_ABLATIONS): the product path plus the
+    PGB_* switchable alternatives.  Loaded only on request, never by the product path."""
+    global _ablation
+    if _ablation is None:
+        if not ABLATION_LIB_PATH.exists():
+            raise ImportError(f"{ABLATION_LIB_PATH} is not built (make -C paper_2512_00398_b200/csrc)")
+        _ablation = _bind(ctypes.CDLL(str(ABLATION_LIB_PATH), mode=os.RTLD_LOCAL))
+    return _ablation
+
+
+def check(rc: int, handle: ctypes.CDLL | None = None) -> None:
+    """Raise the pulsegrid exception named by a pgb_status (message from `handle`'s
+    thread-local last error; default: the product library)."""
     if rc:
-        raise_for(rc, lib.pgb_last_error().decode(errors="replace"))
+        raise_for(rc, (handle or lib).pgb_last_error().decode(errors="replace"))
 
 
 def device_count() -> int:

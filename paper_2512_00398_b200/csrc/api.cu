@@ -158,6 +158,8 @@ struct pgb_context {
     std::vector<std::pair<std::string, cudaEvent_t>> trace_ev;
     std::vector<double> trace_host;  // host clock (ms) when each mark was issued
     DevBuf cl_scratch, clusters, members;
+    DevBuf d_wide;    // rows of trial blocks too wide for the staged dedispersion
+    DevBuf d_levels;  // boxcar ladder levels above the tile kernel's (boxcar_max > 8192)
     PinnedBuf h_counters;
     RfiWork rfi;
     DevBuf rfi_out;
@@ -251,8 +253,8 @@ void validate_cfg(pgb_context* ctx, const pgb_chunk_spec* spec, const pgb_engine
     if (cfg->n_workers < 1) raise(PGB_ERR_CONFIG, "n_workers must be >= 1");
     if (cfg->boxcar_max < 1 || (cfg->boxcar_max & (cfg->boxcar_max - 1)) != 0)
         raise(PGB_ERR_CONFIG, "boxcar_max must be a power of two");
-    if (cfg->boxcar_max > 8192)
-        raise(PGB_ERR_CONFIG, "boxcar_max > 8192 is not supported by the device path");
+    if (cfg->boxcar_max > (1ull << 30))  // ladder levels fit the 5-bit fragment level field
+        raise(PGB_ERR_CONFIG, "boxcar_max above 2^30");
     if (ctx->ntrials == 0) return;
     if (cfg->max_in_flight == 0) {  // in_flight_limit, src/engine.cpp:75-83
         const int64_t min_delay = ctx->maxd[0];
@@ -421,20 +423,29 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     }
     std::vector<uint32_t> blk_len(nblocks, 0);
     for (uint32_t r = 0; r < nrows; ++r) blk_len[r / tb] = std::max(blk_len[r / tb], row_len[r]);
-    const uint32_t spread = *std::max_element(ctx->blk_spread.begin(), ctx->blk_spread.end());
-
     const bool u8 = in.u8;
+    // Blocks whose channel delay spread fits a staged window go through the shared-memory
+    // kernels; wider ones (very coarse DM steps) through the direct kernel, which reads
+    // the channel rows from L1/L2.  The staged kernels skip those (block length 0).
+    uint32_t spread = 0;
+    std::vector<uint32_t> wide_rows;
+    for (uint32_t b = 0; b < nblocks; ++b) {
+        if (dedisp_staged_fits(u8, ctx->blk_spread[b])) {
+            spread = std::max(spread, ctx->blk_spread[b]);
+        } else {
+            for (uint32_t r = b * tb; r < std::min(nrows, (b + 1) * tb); ++r) wide_rows.push_back(r);
+            blk_len[b] = 0;
+        }
+    }
     const uint32_t align_el = u8 ? 16 : 4;
     const uint32_t wmax = (uint32_t)round_up(spread + DD_NT + 2 * align_el + 16, 16);
     int g = 8;
     while (g > 1 && dedisp_smem_bytes(u8, g, wmax) > DD_SMEM_BUDGET) g >>= 1;
-    if (dedisp_smem_bytes(u8, g, wmax) > DD_SMEM_BUDGET || (u8 && (uint64_t)g * wmax / 16 > 4ull * DD_THREADS))
-        raise(PGB_ERR_CONFIG, "per-block channel delay spread of " + std::to_string(spread) +
-                                  " samples exceeds the dedispersion staging capacity");
     // warp-specialized TMA kernel (u8): 16-byte aligned window starts, 256-byte boxes,
     // >= 20 bytes of slack for the packers' funnel shifts; deepest ring that fits
     int ws_g = 0, ws_ns = 0;
     const uint32_t ws_wmax = (uint32_t)round_up(spread + DD_NT + 16 + 20, 2048);
+#ifdef PGB_ABLATIONS
     if (u8 && dedisp_ws_available()) {
         const int cand[][2] = {{8, 4}, {8, 3}, {4, 4}, {4, 3}, {8, 2}, {2, 4}, {4, 2}, {2, 3}, {1, 4}, {1, 2}};
         for (const auto& c : cand)
@@ -443,13 +454,14 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                 ws_ns = c[1];
                 break;
             }
-        const char* eg = getenv("PGB_WS_G");  // geometry overrides (experiments)
-        const char* en = getenv("PGB_WS_NS");
+        const char* eg = pgb_ablation_env("PGB_WS_G");  // geometry overrides (experiments)
+        const char* en = pgb_ablation_env("PGB_WS_NS");
         if (eg && en && dedisp_ws_smem_bytes(atoi(eg), ws_wmax, atoi(en)) <= 220 * 1024) {
             ws_g = atoi(eg);
             ws_ns = atoi(en);
         }
     }
+#endif
     const uint32_t ntiles = (uint32_t)((max_n + DD_NT - 1) / DD_NT);
     const uint64_t out_pitch = std::max<uint64_t>((uint64_t)ntiles * DD_NT, round_up(in.pitch_min, DD_NT));
     const uint64_t rows_pitch =
@@ -477,9 +489,15 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         stage_h2d(ctx, ctx->d_scale.p, sc, sizeof sc, st);
     }
 
+    if (!wide_rows.empty()) {
+        ctx->d_wide.reserve(wide_rows.size() * sizeof(uint32_t));
+        stage_h2d(ctx, ctx->d_wide.p, wide_rows.data(), wide_rows.size() * sizeof(uint32_t), st);
+    }
     // 1. transpose to channel-major rows (a progressive chunk transposes per sub-segment
     // below, interleaved with the dedispersion of the tiles it completes)
-    const bool progressive = u8 && in.prog && !ws_g && !in.prog->empty();
+    const bool progressive = u8 && in.prog && !ws_g && !in.prog->empty() && wide_rows.empty();
+    if (in.prog && !in.prog->empty() && !progressive)  // whole chunk first
+        PGB_CUDA(cudaStreamWaitEvent(st, in.prog->back().second, 0));
     if (u8) {
         if (!progressive)
             launch_transpose_u8(static_cast<const uint8_t*>(in.data), L, C, ctx->rows.as<uint8_t>(),
@@ -510,6 +528,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     dl.mul24 = 1u << 24;
     uint64_t reused = 0;  // channel-adds taken over from the previous chunk
     PGB_CUDA(cudaEventRecord(in.ev0 ? in.ev0 : ctx->ev_dd0[slot], st));
+#ifdef PGB_ABLATIONS
     if (u8 && ws_g) {
         DedispLaunch dw = dl;
         dw.g = ws_g;
@@ -522,7 +541,9 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         launch_ws_offsets(dw, ctx->ws_base.as<uint32_t>(), ctx->ws_off.as<uint16_t>(), st);
         ctx->launches += 1;
         launch_dedisp_u8_ws(dw, ws_ns, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
-    } else if (u8) {
+    } else
+#endif
+    if (u8) {
         dl.nchans_pad = C_pad;
         if (ctx->dd_tab_wmax != wmax) {
             ctx->dd_win.reserve((size_t)nblocks * dl.nchans_pad * sizeof(uint2));
@@ -539,7 +560,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         // the front of each row instead of being summed again.  Every output of chunk k
         // is still a sum over the same input bytes, so the series is unchanged bit for bit.
         if (in.raw && ser_prev && out_pitch == ctx->ser_pitch && spec->start_sample > ctx->ser_start &&
-            !getenv("PGB_NO_OVERLAP_REUSE")) {
+            !pgb_ablation_env("PGB_NO_OVERLAP_REUSE")) {
             const uint64_t shift = spec->start_sample - ctx->ser_start;
             std::vector<uint32_t> keep(nrows);
             uint64_t kmax = 0;
@@ -567,7 +588,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
             }
         }
         // persistent ring kernel: one CTA per SM pulling (block, tile) items from a counter
-        if (!getenv("PGB_DD_PERSIST0")) {
+        if (!pgb_ablation_env("PGB_DD_PERSIST0")) {
             ctx->d_work.reserve(64 * sizeof(uint32_t), true);
             dl.work_ctr = ctx->d_work.as<uint32_t>();
         }
@@ -606,9 +627,11 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                 part.tile0 = done;
                 dd_launch(part);
             }
-        } else {
+        } else if (wide_rows.size() < nrows) {
             dd_launch(dl);
         }
+        launch_dedisp_direct(dl, true, ctx->rows.p, ctx->series.p, ctx->d_wide.as<uint32_t>(),
+                             (uint32_t)wide_rows.size(), st);
         if (in.raw) {
             ctx->ser_ok = true;
             ctx->ser_start = spec->start_sample;
@@ -629,7 +652,9 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
             dl.dd_win = ctx->ddf_win.as<uint2>();
             dl.dd_off = ctx->ddf_off.as<uint32_t>();
         }
-        launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
+        if (wide_rows.size() < nrows) launch_dedisp_f32(dl, ctx->rows.as<float>(), ctx->series.as<float>(), st);
+        launch_dedisp_direct(dl, false, ctx->rows.p, ctx->series.p, ctx->d_wide.as<uint32_t>(),
+                             (uint32_t)wide_rows.size(), st);
     }
     PGB_CUDA(cudaEventRecord(in.ev1 ? in.ev1 : ctx->ev_dd1[slot], st));
     trace_mark(ctx, "dedispersion", st);
@@ -649,7 +674,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         if (u8)
         {
             long long* bsums = nullptr;
-            if (!getenv("PGB_BASELINE_SERIAL")) {
+            if (!pgb_ablation_env("PGB_BASELINE_SERIAL")) {
                 ctx->d_bsums.reserve(baseline_block_sums_bytes(nrows, out_pitch));
                 bsums = ctx->d_bsums.as<long long>();
             }
@@ -660,7 +685,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         {
             long long* bsums = nullptr;
             int* lmin = nullptr;
-            if (!getenv("PGB_BASELINE_SERIAL")) {
+            if (!pgb_ablation_env("PGB_BASELINE_SERIAL")) {
                 ctx->d_bsums.reserve(baseline_block_sums_bytes(nrows, out_pitch));
                 ctx->d_lmin.reserve(nrows * sizeof(int));
                 bsums = ctx->d_bsums.as<long long>();
@@ -673,7 +698,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         kind = 0;
     }
     trace_mark(ctx, "baseline", st);
-    static const bool rms_main = getenv("PGB_RMS_MAIN") != nullptr;  // experiment: no overlap
+    static const bool rms_main = pgb_ablation_env("PGB_RMS_MAIN") != nullptr;  // experiment: no overlap
     cudaStream_t rst = rms_main ? st : ctx->rms_st;
     PGB_CUDA(cudaEventRecord(ctx->ev_front[slot], st));
     PGB_CUDA(cudaStreamWaitEvent(rst, ctx->ev_front[slot], 0));
@@ -691,6 +716,14 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     run.baseline = baseline;
     run.u8 = u8;
     run.work = work;
+}
+
+// Global ladder levels for boxcar_max > BX_TILE_MAX (null otherwise).
+double* box_levels(pgb_context* ctx, uint64_t boxcar_max, uint32_t nrows, uint64_t pitch) {
+    const size_t b = boxcar_levels_bytes(boxcar_max, nrows, pitch);
+    if (!b) return nullptr;
+    ctx->d_levels.reserve(b);
+    return ctx->d_levels.as<double>();
 }
 
 void chunk_back(pgb_context* ctx, ChunkRun& run) {
@@ -731,7 +764,8 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
                             ctx->status[slot].as<uint8_t>(), nrows, out_pitch, max_n, cp,
                             ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
                             ctx->d_scale.as<double>(), ctx->cands_raw.as<pgb_candidate>(), dcnt,
-                            ctx->cand_cap, ctx->frags.as<Fragment>(), dcnt + 1, ctx->frag_cap, st);
+                            ctx->cand_cap, ctx->frags.as<Fragment>(), dcnt + 1, ctx->frag_cap,
+                            box_levels(ctx, cfg->boxcar_max, nrows, out_pitch), st);
         PGB_CUDA(cudaMemcpyAsync(hcnt, dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         PGB_CUDA(cudaStreamSynchronize(st));
         const uint64_t nc = hcnt[0], nf = hcnt[1];
@@ -835,7 +869,8 @@ void chunk_back_async(pgb_context* ctx, ChunkRun& run, uint8_t* h_status, uint64
                         ctx->status[slot].as<uint8_t>(), run.nrows, run.out_pitch, run.max_n, cp,
                         ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
                         ctx->d_scale.as<double>(), ctx->cands_raw.as<pgb_candidate>(), dcnt, ccap,
-                        ctx->frags.as<Fragment>(), dcnt + 1, fcap, st);
+                        ctx->frags.as<Fragment>(), dcnt + 1, fcap,
+                        box_levels(ctx, cfg->boxcar_max, run.nrows, run.out_pitch), st);
     trace_mark(ctx, "boxcar + runs", st);
     sort_fragments_dev(ctx->frags.as<Fragment>(), ctx->frags_sorted.as<Fragment>(), fcap, dcnt + 1,
                        ctx->sort_tmp.p, tmp, ka, ka + cap, ia, ia + cap, st);
@@ -920,7 +955,7 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
 // path: every in-order fp32 partial sum is then an exact integer, so series and
 // baselines are bit-identical.  Repacked on the device; otherwise the fp32 path.
 ChunkInput prepare_f32(pgb_context* ctx, const float* dptr, uint64_t length) {
-    if (!ctx->ntrials || !length || getenv("PGB_FORCE_F32_PATH")) return ChunkInput{dptr, false};
+    if (!ctx->ntrials || !length || pgb_ablation_env("PGB_FORCE_F32_PATH")) return ChunkInput{dptr, false};
     const size_t cells = (size_t)length * ctx->nchans;
     ctx->in_u8.reserve(cells);
     ctx->counters.reserve(4 * sizeof(unsigned long long));
@@ -1103,7 +1138,7 @@ pgb_status pgb_destroy(pgb_context* ctx) {
                           &ctx->rfi.samp_bad, &ctx->rfi.dbl, &ctx->rfi.tmp, &ctx->rfi.rows, &ctx->cands_raw, &ctx->cands_sorted,
                           &ctx->frags, &ctx->frags_sorted, &ctx->counters, &ctx->sort_keys,
                           &ctx->sort_idx, &ctx->sort_tmp, &ctx->payload, &ctx->file_cands,
-                          &ctx->file_sorted, &ctx->cl_scratch, &ctx->clusters, &ctx->members})
+                          &ctx->file_sorted, &ctx->cl_scratch, &ctx->clusters, &ctx->members, &ctx->d_levels, &ctx->d_wide})
             b->release();
         ctx->h_counters.release();
         for (auto e : ctx->seg_events) cudaEventDestroy(e);
@@ -1427,7 +1462,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
             uint64_t done = 0;
             ctx->prog.clear();
             const bool prog_ok = nchunks > 0 && !(rfi && (rfi->narrowband || rfi->broadband)) &&
-                                 chunks[0].start_sample == 0 && !getenv("PGB_NO_PROGRESSIVE");
+                                 chunks[0].start_sample == 0 && !pgb_ablation_env("PGB_NO_PROGRESSIVE");
             if (prog_ok) {
                 const uint64_t L0 = std::min<uint64_t>(chunks[0].length, nsamples);
                 while (ctx->sub_events.size() < PGB_PROG_SUBSEG) {
@@ -1473,7 +1508,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
         ctx->ser_ok = false;
         // Back halves: asynchronous (device-side counts, one read at the end of the file)
         // unless PGB_SYNC_BACK is set (per-chunk host reads, the run_dm_loop path).
-        const bool async_back = !getenv("PGB_SYNC_BACK");
+        const bool async_back = !pgb_ablation_env("PGB_SYNC_BACK");
         uint32_t max_rows = 0;
         for (uint32_t t = ctx->tr_begin; t < ctx->tr_end; ++t) ++max_rows;
         struct ChunkBook {  // what the end-of-file pass needs from each chunk

@@ -21,6 +21,9 @@
 
 #include <algorithm>
 
+#include <cmath>
+#include <utility>
+
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -727,7 +730,7 @@ __global__ void __launch_bounds__(BX_THREADS)
     boxcar_peaks_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len,
                         const float* __restrict__ frms_all, const uint8_t* __restrict__ status,
                         uint64_t pitch, uint64_t bmax, const double* __restrict__ scale,
-                        PeakCtx ctx) {
+                        PeakCtx ctx, double* __restrict__ lvl_out) {
     constexpr int N = BX_THREADS * S;
     // S == 16 (boxcar_max <= 4096): each buffer carries a zero pad of N/4 >= max half so
     // the shifted read needs no bounds test; S == 24 (8192) tests instead (smem limit).
@@ -863,6 +866,69 @@ __global__ void __launch_bounds__(BX_THREADS)
             }
         }
     }
+    // boxcar_max beyond the tile ladder: hand the top level (w = bmax, valid for the
+    // tile's first T outputs) to boxcar_level_kernel through global memory
+    if (lvl_out && n >= bmax) {
+        const uint64_t m = n - bmax + 1;
+        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+        double* dst = lvl_out + base;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const uint32_t j = tid + BX_THREADS * k;
+            if (j < lim2) dst[j] = r[k];
+        }
+    }
+}
+
+// One ladder level above the tile kernel's (boxcar_max > 8192): out[i] = in[i] +
+// in[i + half] for i < m_w = n - w + 1 (the reference's in-place ascending update,
+// src/detect.cpp:216-221, reads the previous level at i + half, so out-of-place is the
+// same), then the threshold runs of the level as in the tile kernel: a thread scans a
+// strip of BXL_S consecutive outputs; runs inside it become candidates, runs touching a
+// strip edge fragments for stitch_kernel.  HBM-bound: 16 B read + 8 B written per output.
+constexpr int BXL_S = 16;
+__global__ void __launch_bounds__(256)
+    boxcar_level_kernel(const double* __restrict__ in, double* __restrict__ out,
+                        const uint32_t* __restrict__ row_len, const uint8_t* __restrict__ status,
+                        uint64_t pitch, uint32_t level, double sc, PeakCtx ctx) {
+    const uint32_t row = blockIdx.x;
+    if (status[row]) return;
+    const uint64_t n = row_len[row];
+    const uint64_t w = 1ull << level, half = w >> 1;
+    if (n < w) return;
+    const uint64_t m = n - w + 1;
+    const uint64_t lo = ((uint64_t)blockIdx.y * blockDim.x + threadIdx.x) * BXL_S;
+    if (lo >= m) return;
+    const uint64_t hi = lo + BXL_S < m ? lo + BXL_S : m;
+    const double* a = in + (size_t)row * pitch;
+    double* o = out + (size_t)row * pitch;
+    const double thr = ctx.cp.threshold;
+    bool in_run = false;
+    uint64_t rb = 0, pk = 0;
+    double pv = 0.0;
+    for (uint64_t j = lo; j < hi; ++j) {
+        const double s = __dadd_rn(a[j], a[j + half]);  // :219
+        o[j] = s;
+        const double v = __dmul_rn(s, sc);
+        if (v > thr) {
+            if (!in_run) {
+                in_run = true;
+                rb = pk = j;
+                pv = v;
+            } else if (v > pv) {
+                pk = j;
+                pv = v;
+            }
+        } else if (in_run) {
+            in_run = false;
+            if (rb == lo && lo > 0) emit_fragment(ctx, row, level, rb, j - 1, pk, pv);
+            else emit_candidate(ctx, row, level, m, rb, j - 1, pk, pv);
+        }
+    }
+    if (in_run) {
+        if ((rb == lo && lo > 0) || hi < m) emit_fragment(ctx, row, level, rb, hi - 1, pk, pv);
+        else emit_candidate(ctx, row, level, m, rb, hi - 1, pk, pv);
+    }
 }
 
 __global__ void stitch_kernel(const Fragment* __restrict__ f, uint64_t nf,
@@ -966,10 +1032,15 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
                          const ChainParams& cp, const uint32_t* active, const double* dms,
                          const double* scale, pgb_candidate* cands, unsigned long long* n_cands,
                          uint64_t cand_cap, Fragment* frags, unsigned long long* n_frags,
-                         uint64_t frag_cap, cudaStream_t st) {
+                         uint64_t frag_cap, double* levels, cudaStream_t st) {
     if (!nrows || !max_len) return;
     PeakCtx ctx{active, dms, cp, cands, n_cands, cand_cap, frags, n_frags, frag_cap};
-    const uint64_t bmax = cp.boxcar_max;
+    // boxcar_max > BX_TILE_MAX: the tile kernel runs the ladder to w = BX_TILE_LADDER and
+    // stores that level; boxcar_level_kernel then doubles in global memory (ping-pong
+    // `levels`, 2 x nrows x pitch doubles) up to boxcar_max
+    const bool ext = cp.boxcar_max > BX_TILE_MAX;
+    const uint64_t bmax = ext ? BX_TILE_LADDER : cp.boxcar_max;
+    double* lvl_out = ext ? levels : nullptr;
     // 2 x N doubles must fit in 227 KB.  A tile yields N - bmax outputs, so for the
     // long ladders S = 24 (N = 12288, 1.5x halo overhead instead of 2x at bmax 4096)
     const int S = bmax <= 2048 ? 16 : 24;
@@ -984,7 +1055,7 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
         PGB_CUDA(cudaFuncSetAttribute(boxcar_peaks_kernel<K, SS>,                            \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
         boxcar_peaks_kernel<K, SS><<<grid, BX_THREADS, smem, st>>>(x, row_len, frms, status, \
-                                                                   pitch, bmax, scale, ctx); \
+                                                                   pitch, bmax, scale, ctx, lvl_out); \
     } while (0)
     if (S == 16) {
         if (kind == 1) PGB_BX(1, 16);
@@ -995,6 +1066,25 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
     }
 #undef PGB_BX
     PGB_CUDA(cudaGetLastError());
+    if (ext) {
+        double* in = levels;
+        double* out = levels + (size_t)nrows * pitch;
+        uint32_t level = 0;
+        while ((1ull << level) < bmax) ++level;
+        for (uint64_t w = bmax << 1; w <= cp.boxcar_max && w <= max_len; w <<= 1) {
+            ++level;
+            const double sc = 1.0 / std::sqrt((double)(1ull << level));  // as the host table (src/engine.cpp:207)
+            const uint64_t per = 256ull * BXL_S;
+            dim3 g2(nrows, (unsigned)((max_len + per - 1) / per));
+            boxcar_level_kernel<<<g2, 256, 0, st>>>(in, out, row_len, status, pitch, level, sc, ctx);
+            PGB_CUDA(cudaGetLastError());
+            std::swap(in, out);
+        }
+    }
+}
+
+size_t boxcar_levels_bytes(uint64_t boxcar_max, uint32_t nrows, uint64_t pitch) {
+    return boxcar_max > BX_TILE_MAX ? 2 * (size_t)nrows * pitch * sizeof(double) : 0;
 }
 
 void launch_stitch(const Fragment* frags_sorted, uint64_t nfrags, const uint32_t* row_len,

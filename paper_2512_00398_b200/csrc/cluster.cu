@@ -490,9 +490,9 @@ void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_r
     cub::DoubleBuffer<uint32_t> cv(idx_a, idx_b);
     PGB_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp, sort_tmp, ck, cv, (int)n, 0, 64, st));
     const int link_mode = [] {  // ablation: PGB_LINK_GLOBAL / PGB_LINK_SMEM1 / PGB_LINK_SMEM2
-        if (getenv("PGB_LINK_GLOBAL")) return 2;
-        if (getenv("PGB_LINK_SMEM1")) return 1;
-        if (getenv("PGB_LINK_SMEM2")) return 3;
+        if (pgb_ablation_env("PGB_LINK_GLOBAL")) return 2;
+        if (pgb_ablation_env("PGB_LINK_SMEM1")) return 1;
+        if (pgb_ablation_env("PGB_LINK_SMEM2")) return 3;
         return 0;
     }();
     if (link_mode == 0) {

@@ -86,6 +86,7 @@ __device__ __forceinline__ void stage_offsets(const DedispLaunch& p, uint32_t d,
 
 constexpr int U8_VPT = 4;  // max 16-byte vectors per thread per stage (host guarantees)
 
+#ifdef PGB_ABLATIONS  // per-stage-offset kernel (HMODE ablations)
 // HMODE selects how the odd samples are accumulated (ablation):
 //   0: H += w >> 8 via __umulhi -> ptxas emits LEA.HI (ALU pipe)
 //   1: H += hi(w * 2^24) via mad.hi (IMAD.HI on the FMA pipe; needs a 64-bit addend pair)
@@ -268,6 +269,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     }
 }
 
+#endif  // PGB_ABLATIONS
 // ---- mbarrier ring variant ---------------------------------------------------------
 // Same tile, table, staging layout and SWAR accumulation as dedisp_u8_tab_kernel, but the
 // CTA-wide barrier per stage is replaced by per-slot mbarriers over a 3-slot ring:
@@ -551,6 +553,7 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
     }
 }
 
+#ifdef PGB_ABLATIONS  // grid-launched ring (the product launches the persistent one)
 template <int G, int VPT, int MODE, int NS = RING_NS>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_u8_ring_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
@@ -562,6 +565,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     ring_tile<G, VPT, MODE, NS>(p, rows, out, blk_len, blk, tile);
 }
 
+#endif  // PGB_ABLATIONS
 // Persistent variant: one CTA per SM takes (block, tile) items from a counter in the
 // grid's order (blocks fastest), so the last wave is not quantised to whole CTAs of a
 // 7-55-wave grid (the tail is ~1 % of a launch with 8192 CTAs, several % with 1024).
@@ -608,6 +612,7 @@ __global__ void dd_table_kernel(const DedispLaunch p, uint2* __restrict__ win, u
         win[gw] = make_uint2(a, (((dmax - a) & ~3u) + DD_NT - 1) / 16 + 1);
 }
 
+#ifdef PGB_ABLATIONS  // CTA-barrier table kernel (SF ablations)
 // Table-driven u8 kernel (default).  Same tile, staging layout and SWAR accumulation as
 // dedisp_u8_kernel<.., 3>, but the per-stage offsets come from dd_table_kernel:
 //   * the per-trial offsets of stage g+1 are copied into shared memory with cp.async
@@ -799,6 +804,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
     }
 }
 
+#endif  // PGB_ABLATIONS
 template <int TPW>
 __global__ void __launch_bounds__(DD_THREADS, 1)
     dedisp_f32_kernel(const DedispLaunch p, const float* __restrict__ rows,
@@ -1126,6 +1132,66 @@ __global__ void pack_u8_kernel(const float* __restrict__ in, size_t cells, uint8
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(not_u8, 1ull);
 }
 
+// ---- direct fallback for wide trial blocks -------------------------------------------
+// A 32-trial block whose channel delay spread is so wide that no staged window fits in
+// shared memory (e.g. DM steps of tens over a 4096-channel L-band: a block spread of
+// 27k samples) is dedispersed straight from the channel rows in global memory (L1/L2):
+// one CTA per (trial, DD_NT-output tile), a thread per 4 consecutive outputs, channels
+// ascending.  u8: two aligned words and a funnel shift per (thread, channel), the same
+// exact SWAR lanes (bytes 0/2 and 1/3 in u16 lanes, decoded every 256 channels).
+// f32: in-order __fadd_rn per output, the reference's rounding sequence.
+__global__ void __launch_bounds__(256)
+    dedisp_u8_direct_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows, int32_t* __restrict__ out,
+                            const uint32_t* __restrict__ wide_rows) {
+    const uint32_t r = wide_rows[blockIdx.x];
+    const uint32_t tile = blockIdx.y + p.tile0;
+    if (p.blk_first && tile < p.blk_first[r / 32]) return;  // shifted in from the previous chunk
+    if ((uint64_t)tile * DD_NT >= p.row_len[r]) return;
+    const uint32_t t = p.active[r];
+    const uint64_t i = (uint64_t)tile * DD_NT + 4 * threadIdx.x;
+    const uint8_t* base = rows + i;
+    uint32_t E = 0, H = 0;
+    int4 acc = make_int4(0, 0, 0, 0);
+    for (uint32_t c0 = 0; c0 < p.nchans; c0 += DD_FLUSH_CH) {
+        const uint32_t c1 = min(p.nchans, c0 + (uint32_t)DD_FLUSH_CH);
+#pragma unroll 4
+        for (uint32_t c = c0; c < c1; ++c) {
+            const uint32_t d = (uint32_t)__ldg(p.delays_ct + (size_t)c * p.ntrials_plan + t);
+            const uintptr_t a = reinterpret_cast<uintptr_t>(base + (size_t)c * p.rows_pitch + d);
+            const uint32_t* w2 = reinterpret_cast<const uint32_t*>(a & ~uintptr_t(3));
+            const uint32_t w = __funnelshift_r(__ldg(w2), __ldg(w2 + 1), (uint32_t)(a & 3) * 8);
+            E += w & 0x00ff00ffu;
+            H += (w >> 8) & 0x00ff00ffu;
+        }
+        acc.x += (int)(E & 0xffffu);
+        acc.y += (int)(H & 0xffffu);
+        acc.z += (int)(E >> 16);
+        acc.w += (int)(H >> 16);
+        E = H = 0;
+    }
+    *reinterpret_cast<int4*>(out + (size_t)r * p.out_pitch + i) = acc;
+}
+
+__global__ void __launch_bounds__(256)
+    dedisp_f32_direct_kernel(const DedispLaunch p, const float* __restrict__ rows, float* __restrict__ out,
+                             const uint32_t* __restrict__ wide_rows) {
+    const uint32_t r = wide_rows[blockIdx.x];
+    const uint32_t tile = blockIdx.y + p.tile0;
+    if ((uint64_t)tile * DD_NT >= p.row_len[r]) return;
+    const uint32_t t = p.active[r];
+    const uint64_t i0 = (uint64_t)tile * DD_NT + threadIdx.x;
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};  // outputs i0 + 256 k: coalesced across the warp
+    for (uint32_t c = 0; c < p.nchans; ++c) {
+        const uint32_t d = (uint32_t)__ldg(p.delays_ct + (size_t)c * p.ntrials_plan + t);
+        const float* src = rows + (size_t)c * p.rows_pitch + i0 + d;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) acc[k] = __fadd_rn(acc[k], __ldg(src + 256 * k));  // src/dedisp.cpp:146-160
+    }
+    float* dst = out + (size_t)r * p.out_pitch + i0;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) dst[256 * k] = acc[k];
+}
+
 }  // namespace
 
 void launch_pack_u8(const float* in, size_t cells, uint8_t* out, unsigned long long* not_u8,
@@ -1160,34 +1226,35 @@ size_t ring_smem_bytes(int g, uint32_t wmax, int ns = RING_NS) {
     return (size_t)ns * g * 4 * wmax + (size_t)ns * g * 32 * 4 + 2 * ns * sizeof(uint64_t);
 }
 
-void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
+#ifdef PGB_ABLATIONS
+void launch_dedisp_u8_ablation(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
     const size_t smem = dedisp_smem_bytes(true, p.g, p.wmax);
     const int tb = DD_WARPS * p.tpw;
     dim3 grid((p.nrows + tb - 1) / tb, p.ntiles - p.tile0);
     static const int mode = [] {
-        const char* e = getenv("PGB_DD_HMODE");
+        const char* e = pgb_ablation_env("PGB_DD_HMODE");
         return e ? atoi(e) : 3;
     }();
     static const bool v1 = [] {  // PGB_DD_V1=1: per-stage offset kernel (ablation)
-        const char* e = getenv("PGB_DD_V1");
+        const char* e = pgb_ablation_env("PGB_DD_V1");
         return e && *e && *e != '0';
     }();
     static const int sf = [] {  // variant bits: 1 = staging shifts on the FMA pipe (ablation),
         // 2 = odd-word H accumulation on the FMA pipe (IMAD.HI) to balance ALU/FMA
-        const char* e = getenv("PGB_DD_SFMA");
-        const char* h = getenv("PGB_DD_HHI");
+        const char* e = pgb_ablation_env("PGB_DD_SFMA");
+        const char* h = pgb_ablation_env("PGB_DD_HHI");
         int v = (e && *e == '1' ? 1 : 0) | (h && *h == '1' ? 2 : 0);
 #ifdef PGB_DD_EXPERIMENTS
-        if (const char* x = getenv("PGB_DD_EXPERIMENT")) v |= atoi(x) & ~3;
+        if (const char* x = pgb_ablation_env("PGB_DD_EXPERIMENT")) v |= atoi(x) & ~3;
 #endif
         return v;
     }();
     static const bool ring = [] {  // PGB_DD_RING=0: CTA-barrier kernel instead of the mbarrier ring
-        const char* e = getenv("PGB_DD_RING");
+        const char* e = pgb_ablation_env("PGB_DD_RING");
         return !(e && *e == '0');
     }();
     static const int rmode = [] {  // PGB_RING_MODE: ring accumulation / ablation bits (see the kernel)
-        const char* e = getenv("PGB_RING_MODE");
+        const char* e = pgb_ablation_env("PGB_RING_MODE");
         return e ? atoi(e) & 31 : 8;  // default: channel-paired (K, T) accumulation (8)
     }();
     if (ring && !v1 && !sf && p.tpw == 2 && p.dd_off) {
@@ -1233,7 +1300,7 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
         const size_t rsm2 = ring_smem_bytes(p.g, p.wmax, 2);
         const uint32_t vstride2 = 32u * (DD_WARPS / p.g);
         const int vpt2 = (int)((p.wmax / 16 + vstride2 - 1) / vstride2);
-        if (pers && rsm2 <= 227 * 1024 && !getenv("PGB_DD_RING2_OFF")) {
+        if (pers && rsm2 <= 227 * 1024 && !pgb_ablation_env("PGB_DD_RING2_OFF")) {
 #define PGB_RING2(G_, V_, M_)                                                                     \
     if (p.g == G_ && vpt2 <= V_ && rmode == M_) {                                                 \
         PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_, 2, M_>,               \
@@ -1296,6 +1363,62 @@ void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, 
     PGB_CUDA(cudaGetLastError());
 }
 
+#endif  // PGB_ABLATIONS
+
+// Product dispatch: the persistent mbarrier-ring kernel with channel-paired SWAR
+// accumulation (MODE 8), 3 slots at the widest stage that fits, else 2 slots at the
+// host's stage width (wide windows, e.g. config C).  The host's geometry (G from the
+// shared-memory budget, at most 4 vectors per staging thread, dedisp_staged_fits)
+// guarantees one of the two fits; blocks beyond it take launch_dedisp_direct.
+void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
+#ifdef PGB_ABLATIONS
+    launch_dedisp_u8_ablation(p, rows, out, st);
+    return;
+#endif
+    if (p.tpw != 2 || !p.dd_off || !p.work_ctr) raise(PGB_ERR_CONFIG, "dedispersion launch without its staging table");
+    int g = 8;
+    while (g > 1 && ring_smem_bytes(g, p.wmax) > 227 * 1024) g >>= 1;
+    const size_t rsm = ring_smem_bytes(g, p.wmax);
+    const int vpt = (int)((p.wmax / 16 + 32u * (DD_WARPS / g) - 1) / (32u * (DD_WARPS / g)));
+    if (rsm <= 227 * 1024 && g >= p.g) {
+#define PGB_RING3(G_, V_)                                                                         \
+    if (g == G_ && vpt <= V_) {                                                                   \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_, RING_NS, 8>,          \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \
+        dedisp_u8_ring_persist_kernel<G_, V_, RING_NS, 8><<<num_sms(), DD_THREADS, rsm, st>>>(    \
+            p, rows, out, p.blk_len);                                                             \
+        dd_which("ring3-persist", G_, V_, 8);                                                     \
+        PGB_CUDA(cudaGetLastError());                                                             \
+        return;                                                                                   \
+    }
+        PGB_RING3(8, 1) PGB_RING3(8, 2) PGB_RING3(8, 4)
+        PGB_RING3(4, 1) PGB_RING3(4, 2) PGB_RING3(4, 4)
+        PGB_RING3(2, 1) PGB_RING3(2, 2) PGB_RING3(2, 4)
+        PGB_RING3(1, 1) PGB_RING3(1, 2) PGB_RING3(1, 4)
+#undef PGB_RING3
+    }
+    const size_t rsm2 = ring_smem_bytes(p.g, p.wmax, 2);
+    const int vpt2 = (int)((p.wmax / 16 + 32u * (DD_WARPS / p.g) - 1) / (32u * (DD_WARPS / p.g)));
+    if (rsm2 <= 227 * 1024) {
+#define PGB_RING2(G_, V_)                                                                         \
+    if (p.g == G_ && vpt2 <= V_) {                                                                \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_, 2, 8>,                \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm2));   \
+        dedisp_u8_ring_persist_kernel<G_, V_, 2, 8><<<num_sms(), DD_THREADS, rsm2, st>>>(         \
+            p, rows, out, p.blk_len);                                                             \
+        dd_which("ring2-persist", G_, V_, 8);                                                     \
+        PGB_CUDA(cudaGetLastError());                                                             \
+        return;                                                                                   \
+    }
+        PGB_RING2(8, 1) PGB_RING2(8, 2) PGB_RING2(8, 4)
+        PGB_RING2(4, 1) PGB_RING2(4, 2) PGB_RING2(4, 4)
+        PGB_RING2(2, 1) PGB_RING2(2, 2) PGB_RING2(2, 4)
+        PGB_RING2(1, 1) PGB_RING2(1, 2) PGB_RING2(1, 4)
+#undef PGB_RING2
+    }
+    raise(PGB_ERR_CONFIG, "no dedispersion kernel for this staging geometry");
+}
+
 void launch_dd_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st) {
     const uint64_t warps = (uint64_t)((p.nrows + 31) / 32) * p.nchans_pad;
     dd_table_kernel<<<(unsigned)((warps * 32 + 255) / 256), 256, 0, st>>>(p, win, off);
@@ -1316,7 +1439,7 @@ void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cud
     const size_t smem = dedisp_smem_bytes(false, p.g, p.wmax);
     const int tb = DD_WARPS * p.tpw;
     dim3 grid((p.nrows + tb - 1) / tb, p.ntiles);
-    if (p.tpw == 2 && p.dd_off && !getenv("PGB_F32_RING0")) {  // the f32 ring (table built)
+    if (p.tpw == 2 && p.dd_off && !pgb_ablation_env("PGB_F32_RING0")) {  // the f32 ring (table built)
         int g = 8;
         while (g > 1 && fring_smem_bytes(g, p.wmax) > 227 * 1024) g >>= 1;
         const size_t rsm = fring_smem_bytes(g, p.wmax);
@@ -1345,6 +1468,25 @@ void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cud
     PGB_CUDA(cudaGetLastError());
 }
 
+void launch_dedisp_direct(const DedispLaunch& p, bool u8, const void* rows, void* out,
+                          const uint32_t* wide_rows, uint32_t nwide, cudaStream_t st) {
+    if (!nwide || p.ntiles <= p.tile0) return;
+    dim3 grid(nwide, p.ntiles - p.tile0);
+    if (u8)
+        dedisp_u8_direct_kernel<<<grid, 256, 0, st>>>(p, static_cast<const uint8_t*>(rows),
+                                                     static_cast<int32_t*>(out), wide_rows);
+    else
+        dedisp_f32_direct_kernel<<<grid, 256, 0, st>>>(p, static_cast<const float*>(rows),
+                                                      static_cast<float*>(out), wide_rows);
+    PGB_CUDA(cudaGetLastError());
+}
+
+bool dedisp_staged_fits(bool u8, uint32_t spread) {
+    const uint32_t align_el = u8 ? 16 : 4;
+    const uint32_t wmax = (uint32_t)((spread + DD_NT + 2 * align_el + 16 + 15) / 16 * 16);
+    return dedisp_smem_bytes(u8, 1, wmax) <= DD_SMEM_BUDGET && (!u8 || wmax / 16 <= 4u * DD_THREADS);
+}
+
 void launch_series_shift(int32_t* series, uint32_t nrows, uint64_t pitch, uint64_t shift,
                          const uint32_t* keep, cudaStream_t st) {
     if (!nrows) return;
@@ -1355,7 +1497,7 @@ void launch_series_shift(int32_t* series, uint32_t nrows, uint64_t pitch, uint64
 void launch_transpose_u8(const uint8_t* in, uint64_t length, uint32_t nchans, uint8_t* rows,
                          uint64_t pitch, cudaStream_t st) {
     static const int tt = [] {  // PGB_TRANSPOSE_TT: time-tile ablation (64 / 128 / 256)
-        const char* e = getenv("PGB_TRANSPOSE_TT");
+        const char* e = pgb_ablation_env("PGB_TRANSPOSE_TT");
         const int v = e ? atoi(e) : 256;
         return v == 64 || v == 128 ? v : 256;
     }();

@@ -22,6 +22,7 @@
 // Global traffic stays one byte per staged sample (the channel-major rows), so the
 // L2 working set is the same as the classic kernel's; warps drift freely and the
 // ring hides the TMA latency.
+#ifdef PGB_ABLATIONS  // the whole warp-specialised TMA variant is an ablation
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -304,7 +305,7 @@ size_t dedisp_ws_smem_bytes(int g, uint32_t wmax, int nslot) {
 
 // Opt-in (PGB_DD_WS=1): on config B chunks this kernel measures 79 ms against the
 // classic kernel's 66.5 ms ("ablations"), so it is not the default.
-bool dedisp_ws_available() { return encode_fn() != nullptr && getenv("PGB_DD_WS") != nullptr; }
+bool dedisp_ws_available() { return encode_fn() != nullptr && pgb_ablation_env("PGB_DD_WS") != nullptr; }
 
 void launch_ws_offsets(const DedispLaunch& p, uint32_t* wbase, uint16_t* woff, cudaStream_t st) {
     const uint32_t nblocks = (p.nrows + WS_TB - 1) / WS_TB;
@@ -340,3 +341,5 @@ void launch_dedisp_u8_ws(const DedispLaunch& p, int nslot, const uint8_t* rows, 
 }
 
 }  // namespace pgb
+
+#endif  // PGB_ABLATIONS

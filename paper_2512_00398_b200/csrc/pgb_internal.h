@@ -9,6 +9,21 @@
 
 #include "../../include/pulsegrid_b200.h"
 
+// Ablation switches (alternative kernels and schedules compared in DESIGN.md section 10)
+// are read from the environment only by the ablation build, libpgb200_ablations.so
+// (-DPGB_ABLATIONS); the product library never consults them, so no stray variable
+// can change its code path.  Diagnostics (PGB_TRACE, PGB_DD_WHICH) and the initial
+// buffer capacity (PGB_INITIAL_CAP, never changes results) are read by both.
+#include <cstdlib>
+inline const char* pgb_ablation_env(const char* name) {
+#ifdef PGB_ABLATIONS
+    return std::getenv(name);
+#else
+    (void)name;
+    return nullptr;
+#endif
+}
+
 namespace pgb {
 
 // ---- errors -----------------------------------------------------------------
@@ -55,6 +70,11 @@ constexpr size_t DD_SMEM_BUDGET = 200 * 1024;
 
 // Boxcar/peak CTA: buffer of BX_N doubles, BX_THREADS threads.
 constexpr int BX_THREADS = 512;
+// boxcar_max <= BX_TILE_MAX: the whole ladder in one shared-memory tile; above it the
+// tile kernel stops at BX_TILE_LADDER and boxcar_level_kernel continues in global memory
+constexpr uint64_t BX_TILE_MAX = 8192;
+constexpr uint64_t BX_TILE_LADDER = 4096;
+size_t boxcar_levels_bytes(uint64_t boxcar_max, uint32_t nrows, uint64_t pitch);
 
 // Packed fragment of an above-threshold run that touches a strip edge.
 struct Fragment {
@@ -131,6 +151,11 @@ void launch_ddf_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStre
 void launch_series_shift(int32_t* series, uint32_t nrows, uint64_t pitch, uint64_t shift,
                          const uint32_t* keep, cudaStream_t st);
 size_t dedisp_smem_bytes(bool u8, int g, uint32_t wmax);
+// whether a 32-trial block with this channel delay spread fits the staged kernels
+bool dedisp_staged_fits(bool u8, uint32_t spread);
+// blocks that do not: wide_rows lists their rows (every row of each such block)
+void launch_dedisp_direct(const DedispLaunch& p, bool u8, const void* rows, void* out,
+                          const uint32_t* wide_rows, uint32_t nwide, cudaStream_t st);
 // warp-specialized TMA variant (dedisp_tma.cu); p.wmax (bytes) must be a multiple of 256
 void launch_dedisp_u8_ws(const DedispLaunch& p, int nslot, const uint8_t* rows, int32_t* out,
                          cudaStream_t st);
@@ -158,7 +183,7 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
                          uint64_t max_len, const ChainParams& cp, const uint32_t* active,
                          const double* dms, const double* scale, pgb_candidate* cands, unsigned long long* n_cands,
                          uint64_t cand_cap, Fragment* frags, unsigned long long* n_frags,
-                         uint64_t frag_cap, cudaStream_t st);
+                         uint64_t frag_cap, double* levels, cudaStream_t st);
 void launch_stitch(const Fragment* frags_sorted, uint64_t nfrags, const uint32_t* row_len,
                    const ChainParams& cp, const uint32_t* active, const double* dms,
                    pgb_candidate* cands, unsigned long long* n_cands, uint64_t cand_cap,

@@ -340,7 +340,7 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
     if (rp.narrowband) {          // src/rfi.cpp:32-68
         if (nch < 4) raise(PGB_ERR_INSUFFICIENT, "narrowband flagging needs at least 4 channels");
         if (n == 0) raise(PGB_ERR_INSUFFICIENT, "empty chunk");
-        if (std::is_same<T, uint8_t>::value && nch % 16 == 0 && !getenv("PGB_RFI_SERIAL")) {
+        if (std::is_same<T, uint8_t>::value && nch % 16 == 0 && !pgb_ablation_env("PGB_RFI_SERIAL")) {
             auto* sums = reinterpret_cast<unsigned long long*>(s1);  // scratch until median_mad
             PGB_CUDA(cudaMemsetAsync(sums, 0, sizeof(unsigned long long) * nch, st));
             const uint32_t gx = (nch / 4 + 255) / 256;
@@ -364,7 +364,7 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
         chan_flags_kernel<<<nblk(nch), 256, 0, st>>>(a, b, nch, stats, rp.k_mad, w.chan_bad.as<uint8_t>());
     }
     if (rp.broadband && n > 0) {  // src/rfi.cpp:70-91
-        if (std::is_same<T, uint8_t>::value && nch % 16 == 0 && !getenv("PGB_RFI_SERIAL"))
+        if (std::is_same<T, uint8_t>::value && nch % 16 == 0 && !pgb_ablation_env("PGB_RFI_SERIAL"))
             zero_dm_u8_kernel<<<(unsigned)((n * 32 + 255) / 256), 256, 0, st>>>(reinterpret_cast<const uint8_t*>(x),
                                                                                 n, nch, a);
         else
@@ -386,7 +386,7 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
     for (auto v : cb) nbc += v;
     *n_bad_ch = nbc;
     *n_bad_s = nrows_bad;
-    const bool rows4 = nch % 4 == 0 && !getenv("PGB_RFI_SERIAL");
+    const bool rows4 = nch % 4 == 0 && !pgb_ablation_env("PGB_RFI_SERIAL");
     if (rows4)  // bad channels zeroed while widening
         widen_rows_kernel<T><<<148 * 16, 256, 0, st>>>(x, n, nch, w.chan_bad.as<uint8_t>(), out);
     else

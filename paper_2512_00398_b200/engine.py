@@ -23,7 +23,7 @@ from typing import Callable
 import numpy as np
 
 from . import abi
-from ._native import check, lib
+from ._native import ablation_lib, check, lib
 from .dedisp import DmTrialPlan
 
 
@@ -218,18 +218,25 @@ def _device_tensor(x):
 class Engine:
     """One libpgb200 context: a CUDA stream plus a device arena on one GPU."""
 
-    def __init__(self, device: int = 0):
+    def __init__(self, device: int = 0, *, ablations: bool = False):
+        """ablations=True binds libpgb200_ablations.so instead of the product library: the
+        same path plus the alternative kernels and schedules of DESIGN.md section 10,
+        selected by PGB_* environment switches (tests and tools only)."""
         self.device = device
+        self._lib = ablation_lib() if ablations else lib
         h = ctypes.c_void_p()
-        check(lib.pgb_create(int(device), ctypes.byref(h)))
+        self._check(self._lib.pgb_create(int(device), ctypes.byref(h)))
         self._h = h
         self._plan_key = None
         self._range = None
 
+    def _check(self, rc: int) -> None:
+        check(rc, self._lib)
+
     # ---- lifecycle -----------------------------------------------------------
     def close(self) -> None:
         if self._h:
-            lib.pgb_destroy(self._h)
+            self._lib.pgb_destroy(self._h)
             self._h = None
 
     def __del__(self):  # pragma: no cover - interpreter teardown order
@@ -248,14 +255,14 @@ class Engine:
     def set_plan(self, plan: DmTrialPlan, trial_range: tuple[int, int] | None = None) -> None:
         key = (id(plan), plan.ntrials, plan.nchans, plan.delays.ctypes.data)
         if key != self._plan_key:
-            check(lib.pgb_set_plan(self._h, abi.ptr(plan.dms), abi.ptr(plan.delays),
+            self._check(self._lib.pgb_set_plan(self._h, abi.ptr(plan.dms), abi.ptr(plan.delays),
                                    plan.ntrials, plan.nchans))
             self._plan_key = key
             self._plan_ref = plan  # keep the arrays alive while the key is cached
             self._range = None
         rng = trial_range if trial_range is not None else (0, plan.ntrials)
         if rng != self._range:
-            check(lib.pgb_set_trial_range(self._h, int(rng[0]), int(rng[1])))
+            self._check(self._lib.pgb_set_trial_range(self._h, int(rng[0]), int(rng[1])))
             self._range = rng
 
     # ---- run_dm_loop -------------------------------------------------------------
@@ -272,7 +279,7 @@ class Engine:
             import torch
 
             torch.cuda.current_stream().synchronize()
-            fn = lib.pgb_run_dm_loop_u8 if is_u8 else lib.pgb_run_dm_loop_f32
+            fn = self._lib.pgb_run_dm_loop_u8 if is_u8 else self._lib.pgb_run_dm_loop_f32
             check(fn(self._h, ctypes.c_void_p(ptr), 1, ctypes.byref(spec), ctypes.byref(ccfg),
                      ctypes.byref(nc), ctypes.byref(ns)))
         else:
@@ -283,16 +290,16 @@ class Engine:
                 raise ValueError("chunk data shorter than spec.length")
             if data.dtype == np.uint8:
                 data = np.ascontiguousarray(data)
-                fn = lib.pgb_run_dm_loop_u8
+                fn = self._lib.pgb_run_dm_loop_u8
             else:
                 data = np.ascontiguousarray(data, dtype=np.float32)
-                fn = lib.pgb_run_dm_loop_f32
+                fn = self._lib.pgb_run_dm_loop_f32
             check(fn(self._h, abi.ptr(data), 0, ctypes.byref(spec), ctypes.byref(ccfg),
                      ctypes.byref(nc), ctypes.byref(ns)))
         cands = np.zeros(nc.value, abi.CANDIDATE_DTYPE)
-        check(lib.pgb_fetch_candidates(self._h, abi.ptr(cands), nc.value))
+        self._check(self._lib.pgb_fetch_candidates(self._h, abi.ptr(cands), nc.value))
         skipped = np.zeros(ns.value, np.uint64)
-        check(lib.pgb_fetch_skipped(self._h, abi.ptr(skipped), ns.value))
+        self._check(self._lib.pgb_fetch_skipped(self._h, abi.ptr(skipped), ns.value))
         if cfg.timing_sink is not None:
             ms, _, _ = self.last_dedisp_time()
             lo, hi = self._range
@@ -312,10 +319,10 @@ class Engine:
         out = np.zeros((max(0, e - b), L), np.float32)
         if data.dtype == np.uint8:
             data = np.ascontiguousarray(data)
-            fn = lib.pgb_dedisperse_u8
+            fn = self._lib.pgb_dedisperse_u8
         else:
             data = np.ascontiguousarray(data, dtype=np.float32)
-            fn = lib.pgb_dedisperse_f32
+            fn = self._lib.pgb_dedisperse_f32
         check(fn(self._h, abi.ptr(data), L, b, e, abi.ptr(out), L))
         return [out[r, : L - plan.trial_max_delay(b + r)] for r in range(e - b)]
 
@@ -330,7 +337,7 @@ class Engine:
         if dev is not None:
             raise TypeError("pass device candidates through Engine.link_device()")
         arr = np.ascontiguousarray(cands, abi.CANDIDATE_DTYPE)
-        check(lib.pgb_link_grid(self._h, abi.ptr(arr), 0, len(arr), ctypes.byref(r), ctypes.byref(n)))
+        self._check(self._lib.pgb_link_grid(self._h, abi.ptr(arr), 0, len(arr), ctypes.byref(r), ctypes.byref(n)))
         return self._fetch_clusters(n.value, len(arr))
 
     def link_last(self, radii: LinkRadii | None = None) -> "Clusters":
@@ -338,8 +345,8 @@ class Engine:
         radii = radii or LinkRadii()
         r = radii._c()
         p, cnt, n = ctypes.c_void_p(), ctypes.c_size_t(), ctypes.c_size_t()
-        check(lib.pgb_device_candidates(self._h, ctypes.byref(p), ctypes.byref(cnt)))
-        check(lib.pgb_link_grid(self._h, p, 1, cnt.value, ctypes.byref(r), ctypes.byref(n)))
+        self._check(self._lib.pgb_device_candidates(self._h, ctypes.byref(p), ctypes.byref(cnt)))
+        self._check(self._lib.pgb_link_grid(self._h, p, 1, cnt.value, ctypes.byref(r), ctypes.byref(n)))
         return self._fetch_clusters(n.value, cnt.value)
 
     def _fetch_clusters(self, ncl: int, nmem: int) -> "Clusters":
@@ -347,7 +354,7 @@ class Engine:
 
         recs = np.zeros(ncl, abi.CLUSTER_DTYPE)
         members = np.zeros(nmem, np.uint64)
-        check(lib.pgb_fetch_clusters(self._h, abi.ptr(recs), ncl, abi.ptr(members), nmem))
+        self._check(self._lib.pgb_fetch_clusters(self._h, abi.ptr(recs), ncl, abi.ptr(members), nmem))
         return Clusters(recs, members)
 
     # ---- file-level search ------------------------------------------------------------
@@ -380,7 +387,7 @@ class Engine:
         if len(shape) != 2 or shape[1] != plan.nchans or shape[0] < nsamples:
             raise ValueError(f"payload of shape {shape} does not hold {nsamples} x {plan.nchans} samples")
         rc = rfi._c() if (rfi is not None and rfi.active) else None
-        check(lib.pgb_search_file_u8(self._h, ptr, on_dev, int(nsamples), abi.ptr(arr), len(arr),
+        self._check(self._lib.pgb_search_file_u8(self._h, ptr, on_dev, int(nsamples), abi.ptr(arr), len(arr),
                                      ctypes.byref(ccfg), rp, ctypes.byref(rc) if rc is not None else None,
                                      ctypes.byref(nc), ctypes.byref(ncl)))
         return self.fetch_file_results(nc.value, ncl.value)
@@ -404,7 +411,7 @@ class Engine:
         ccfg = cfg._c()
         r = cfg.radii._c()
         rc = rfi._c() if (rfi is not None and rfi.active) else None
-        check(lib.pgb_stream_begin(self._h, int(nsamples), abi.ptr(arr), len(arr), ctypes.byref(ccfg),
+        self._check(self._lib.pgb_stream_begin(self._h, int(nsamples), abi.ptr(arr), len(arr), ctypes.byref(ccfg),
                                    ctypes.byref(r) if cluster else None,
                                    ctypes.byref(rc) if rc is not None else None))
         C = plan.nchans
@@ -412,7 +419,7 @@ class Engine:
 
         def fill(k: int) -> None:
             p, cap = ctypes.c_void_p(), ctypes.c_size_t()
-            check(lib.pgb_stream_buffer(self._h, k, ctypes.byref(p), ctypes.byref(cap)))
+            self._check(self._lib.pgb_stream_buffer(self._h, k, ctypes.byref(p), ctypes.byref(cap)))
             nbytes = chunks[k].length * C
             buf = (ctypes.c_uint8 * nbytes).from_address(p.value)
             mv = memoryview(buf).cast("B")
@@ -436,19 +443,19 @@ class Engine:
                     fut.result()
                     if k + 1 < len(chunks):
                         fut = reader.submit(fill, k + 1)
-                    check(lib.pgb_stream_push(self._h, k, None))
+                    self._check(self._lib.pgb_stream_push(self._h, k, None))
         finally:
             pool.shutdown()
         nc, ncl = ctypes.c_size_t(), ctypes.c_size_t()
-        check(lib.pgb_stream_finish(self._h, ctypes.byref(nc), ctypes.byref(ncl)))
+        self._check(self._lib.pgb_stream_finish(self._h, ctypes.byref(nc), ctypes.byref(ncl)))
         return self.fetch_file_results(nc.value, ncl.value)
 
     def copy_async(self, dst: int, src: int, nbytes: int) -> None:
         """cudaMemcpyAsync on this context's stream (host, device or peer pointers)."""
-        check(lib.pgb_copy_async(self._h, ctypes.c_void_p(dst), ctypes.c_void_p(src), int(nbytes)))
+        self._check(self._lib.pgb_copy_async(self._h, ctypes.c_void_p(dst), ctypes.c_void_p(src), int(nbytes)))
 
     def synchronize(self) -> None:
-        check(lib.pgb_synchronize(self._h))
+        self._check(self._lib.pgb_synchronize(self._h))
 
     # ---- RFI excision --------------------------------------------------------------------
     def rfi_clean(self, chunk_data: np.ndarray, plan: DmTrialPlan, rfi: RfiConfig):
@@ -463,37 +470,37 @@ class Engine:
         out = np.zeros((L, nch), np.float32)
         rc = rfi._c()
         nbc, nbs = ctypes.c_uint64(), ctypes.c_uint64()
-        check(lib.pgb_rfi_clean(self._h, abi.ptr(data), int(is_u8), 0, L, ctypes.byref(rc), abi.ptr(out),
+        self._check(self._lib.pgb_rfi_clean(self._h, abi.ptr(data), int(is_u8), 0, L, ctypes.byref(rc), abi.ptr(out),
                                 ctypes.byref(nbc), ctypes.byref(nbs)))
         bc = np.zeros(nch, np.uint8)
         bs = np.zeros(L, np.uint8)
-        check(lib.pgb_fetch_rfi_flags(self._h, abi.ptr(bc), abi.ptr(bs)))
+        self._check(self._lib.pgb_fetch_rfi_flags(self._h, abi.ptr(bc), abi.ptr(bs)))
         return out, bc.astype(bool), bs.astype(bool)
 
     def fetch_file_results(self, nc: int, ncl: int):
         cands = np.zeros(nc, abi.CANDIDATE_DTYPE)
-        check(lib.pgb_fetch_file_candidates(self._h, abi.ptr(cands), nc))
+        self._check(self._lib.pgb_fetch_file_candidates(self._h, abi.ptr(cands), nc))
         clusters = self._fetch_clusters(ncl, nc)
         npairs = ctypes.c_size_t()
-        check(lib.pgb_fetch_file_skipped(self._h, None, 0, ctypes.byref(npairs)))
+        self._check(self._lib.pgb_fetch_file_skipped(self._h, None, 0, ctypes.byref(npairs)))
         pairs = np.zeros((npairs.value, 2), np.uint64)
-        check(lib.pgb_fetch_file_skipped(self._h, abi.ptr(pairs), npairs.value, ctypes.byref(npairs)))
+        self._check(self._lib.pgb_fetch_file_skipped(self._h, abi.ptr(pairs), npairs.value, ctypes.byref(npairs)))
         return cands, clusters, pairs
 
     # ---- instrumentation ------------------------------------------------------------------
     def launch_count(self) -> int:
         v = ctypes.c_uint64()
-        check(lib.pgb_launch_count(self._h, ctypes.byref(v)))
+        self._check(self._lib.pgb_launch_count(self._h, ctypes.byref(v)))
         return v.value
 
     def last_dedisp_time(self) -> tuple[float, int, int]:
         ms, n, adds = ctypes.c_double(), ctypes.c_uint64(), ctypes.c_uint64()
-        check(lib.pgb_last_dedisp_time(self._h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(adds)))
+        self._check(self._lib.pgb_last_dedisp_time(self._h, ctypes.byref(ms), ctypes.byref(n), ctypes.byref(adds)))
         return ms.value, n.value, adds.value
 
     def stream_handle(self) -> int:
         p = ctypes.c_void_p()
-        check(lib.pgb_stream(self._h, ctypes.byref(p)))
+        self._check(self._lib.pgb_stream(self._h, ctypes.byref(p)))
         return p.value or 0
 
 

@@ -61,3 +61,14 @@ def engine():
     eng = Engine(0)
     yield eng
     eng.close()
+
+
+@pytest.fixture(scope="session")
+def abl_engine():
+    """A context of libpgb200_ablations.so: the PGB_* switchable alternatives (DESIGN.md
+    section 10), compared against the product library's default path."""
+    from paper_2512_00398_b200.engine import Engine
+
+    eng = Engine(0, ablations=True)
+    yield eng
+    eng.close()

@@ -103,3 +103,18 @@ def test_status_codes_map_to_reference_exceptions():
     with pytest.raises(errors.ConfigError):
         errors.raise_for(abi.ERR_CONFIG, "x")
     errors.raise_for(abi.OK, "")
+
+
+def test_product_library_reads_no_ablation_switches():
+    """The alternative kernels and schedules of DESIGN.md section 10 are selected by PGB_*
+    environment variables only in libpgb200_ablations.so; the product library references
+    just the diagnostics (trace, kernel-choice log) and the initial buffer capacity."""
+    import re
+
+    from paper_2512_00398_b200._native import ABLATION_LIB_PATH, LIB_PATH
+
+    names = set(re.findall(rb"PGB_[A-Z0-9_]+", LIB_PATH.read_bytes()))
+    assert names <= {b"PGB_TRACE", b"PGB_DD_WHICH", b"PGB_INITIAL_CAP"}, names
+    if ABLATION_LIB_PATH.exists():
+        abl = set(re.findall(rb"PGB_[A-Z0-9_]+", ABLATION_LIB_PATH.read_bytes()))
+        assert {b"PGB_NO_OVERLAP_REUSE", b"PGB_RING_MODE", b"PGB_SYNC_BACK"} <= abl

@@ -82,7 +82,7 @@ def test_config_b_whole_file_recovers_pulses(engine):
     assert checked >= 5
 
 
-def test_config_b_overlap_reuse_is_exact(engine, monkeypatch):
+def test_config_b_overlap_reuse_is_exact(engine, abl_engine, monkeypatch):
     """search_file moves the outputs chunk k-1 already dedispersed into chunk k instead of
     summing them again; the candidate list must equal the recompute-everything run."""
     import bench
@@ -93,8 +93,8 @@ def test_config_b_overlap_reuse_is_exact(engine, monkeypatch):
     a, ca, _ = engine.search_file(payload, cfg["nsamples"], task.chunks, task.plan, task.engine)
     _, _, adds_reuse = engine.last_dedisp_time()
     monkeypatch.setenv("PGB_NO_OVERLAP_REUSE", "1")
-    b, cb, _ = engine.search_file(payload, cfg["nsamples"], task.chunks, task.plan, task.engine)
-    _, _, adds_full = engine.last_dedisp_time()
+    b, cb, _ = abl_engine.search_file(payload, cfg["nsamples"], task.chunks, task.plan, task.engine)
+    _, _, adds_full = abl_engine.last_dedisp_time()
     assert adds_reuse < 0.96 * adds_full  # the reuse actually happened
     assert len(a) == len(b) > 0
     for k in a.dtype.names:

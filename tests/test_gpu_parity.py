@@ -180,7 +180,7 @@ def test_run_dm_loop_f32_engine_workload(engine, ref):
 
 
 @pytest.mark.parametrize("window", [2001, 40001])
-def test_f32_baseline_exact_and_replayed_rows(engine, ref, monkeypatch, window):
+def test_f32_baseline_exact_and_replayed_rows(abl_engine, engine, ref, monkeypatch, window):
     """Float chunk of multiples of 1/8 (every trial's window sums exact in double -> the
     fixed-point baseline) with one fine-grained sample late in the zero-delay channel:
     trials short enough to exclude it stay exact, the rest take the sequential replay.
@@ -198,7 +198,7 @@ def test_f32_baseline_exact_and_replayed_rows(engine, ref, monkeypatch, window):
     assert len(want) > 0
     a = engine.run_dm_loop(Chunk(spec, g), plan, cfg)
     monkeypatch.setenv("PGB_BASELINE_SERIAL", "1")
-    b = engine.run_dm_loop(Chunk(spec, g), plan, cfg)
+    b = abl_engine.run_dm_loop(Chunk(spec, g), plan, cfg)
     for r in (a, b):
         assert_same_candidates(r.candidates, want)
         assert np.array_equal(r.skipped_trials, want_sk)
@@ -219,7 +219,7 @@ def test_f32_baseline_subnormal_fixed_point(engine, ref):
     assert np.array_equal(res.skipped_trials, want_sk)
 
 
-def test_widened_u8_chunk_takes_integer_path(engine, port, monkeypatch):
+def test_widened_u8_chunk_takes_integer_path(abl_engine, engine, port, monkeypatch):
     """A float chunk of 8-bit codes (read_chunk's widening) is repacked on the device;
     results equal the u8 path, the forced fp32 path and the oracle."""
     hdr, plan, data = _small_u8_case()
@@ -228,7 +228,7 @@ def test_widened_u8_chunk_takes_integer_path(engine, port, monkeypatch):
     a = engine.run_dm_loop(Chunk(spec, data), plan, cfg)
     b = engine.run_dm_loop(Chunk(spec, data.astype(np.float32)), plan, cfg)
     monkeypatch.setenv("PGB_FORCE_F32_PATH", "1")
-    c = engine.run_dm_loop(Chunk(spec, data.astype(np.float32)), plan, cfg)
+    c = abl_engine.run_dm_loop(Chunk(spec, data.astype(np.float32)), plan, cfg)
     want, _ = port.run_dm_loop(data, vars(spec), plan.dms, plan.delays, cfg_dict(cfg))
     for r in (a, b, c):
         assert_same_candidates(r.candidates, want)
@@ -304,7 +304,7 @@ def test_link_grid_vs_reference_library(engine, ref):
 
 @pytest.mark.parametrize("n,extent", [(3000, 20_000), (5120, 200_000), (12288, 2_000_000),
                                       (20000, 3_000_000)])
-def test_link_grid_smem_and_global_forests_agree(engine, port, monkeypatch, n, extent):
+def test_link_grid_smem_and_global_forests_agree(abl_engine, engine, port, monkeypatch, n, extent):
     """link_grid's linking variants -- warp per candidate over a global forest (default),
     one CTA with everything staged in shared memory (<= 5120), one CTA with a shared-memory
     forest (<= 12288), thread per candidate over a global forest -- must all give the
@@ -315,7 +315,7 @@ def test_link_grid_smem_and_global_forests_agree(engine, port, monkeypatch, n, e
     clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)  # warp per candidate
     for mode in ("PGB_LINK_SMEM2", "PGB_LINK_SMEM1", "PGB_LINK_GLOBAL"):
         monkeypatch.setenv(mode, "1")
-        clusters_equal(engine.link_grid(cands, LinkRadii()), recs, members)
+        clusters_equal(abl_engine.link_grid(cands, LinkRadii()), recs, members)
         monkeypatch.delenv(mode)
 
 

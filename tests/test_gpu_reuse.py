@@ -1,13 +1,13 @@
 """Overlap reuse in the file search: the outputs chunk k-1 already dedispersed for the
 samples chunk k shares with it are moved, not summed again.  With and without the reuse
-(PGB_NO_OVERLAP_REUSE=1) the file's candidates and clusters must be identical, with the
+(PGB_NO_OVERLAP_REUSE=1 in the ablation library) the file's candidates and clusters must be identical, with the
 baseline on (chain reads the slot's baseline buffer) and off (chain reads the series)."""
 import numpy as np
 import pytest
 
 from paper_2512_00398_b200.dedisp import FilterbankHeader, LinearSpacing
-from paper_2512_00398_b200.engine import EngineConfig, RfiConfig, default_engine
-from paper_2512_00398_b200.pipeline import SearchParams, create_task, search_file, write_candidates
+from paper_2512_00398_b200.engine import Engine, EngineConfig, RfiConfig, default_engine
+from paper_2512_00398_b200.pipeline import SearchParams, SearchResult, create_task, search_file, write_candidates
 
 from .helpers import u8_chunk
 
@@ -30,8 +30,10 @@ def test_reuse_matches_full_recompute(monkeypatch, baseline_s):
     a = search_file(payload, task)
     adds_a = default_engine(0).last_dedisp_time()[2]
     monkeypatch.setenv("PGB_NO_OVERLAP_REUSE", "1")
-    b = search_file(payload, task)
-    adds_b = default_engine(0).last_dedisp_time()[2]
+    with Engine(0, ablations=True) as abl:
+        cb, clb, _ = abl.search_file(payload, hdr.nsamples, task.chunks, task.plan, task.engine)
+        adds_b = abl.last_dedisp_time()[2]
+    b = SearchResult(cb, clb, None)
     assert adds_a < 0.95 * adds_b  # the reuse actually happened
     assert len(a.candidates) == len(b.candidates) > 0
     for k in a.candidates.dtype.names:
@@ -54,7 +56,9 @@ def test_progressive_first_chunk_matches(monkeypatch):
                        pulses=[(30, 9000, 4, 25.0), (100, 40000, 16, 20.0), (140, 70000, 64, 30.0)])
     a = search_file(payload, task)
     monkeypatch.setenv("PGB_NO_PROGRESSIVE", "1")
-    b = search_file(payload, task)
+    with Engine(0, ablations=True) as abl:
+        cb, clb, _ = abl.search_file(payload, hdr.nsamples, task.chunks, task.plan, task.engine)
+    b = SearchResult(cb, clb, None)
     monkeypatch.delenv("PGB_NO_PROGRESSIVE")
     c = search_file(torch.from_numpy(payload).cuda(), task)
     assert len(a.candidates) > 0
@@ -70,8 +74,6 @@ def test_async_back_halves_match_sync(monkeypatch, initial_cap):
     """The file search's back halves run without host round trips (device-side counts,
     one read per file); the result must equal the per-chunk synchronous path
     (PGB_SYNC_BACK=1), also when tiny initial buffers force the overflow-and-retry path."""
-    from paper_2512_00398_b200.engine import Engine
-
     hdr = FilterbankHeader(fch1=1500.0, foff=-1.0, nchans=256, tsamp=64e-6, nsamples=3 << 15)
     params = SearchParams(dm_lo=0.0, dm_hi=300.0, spacing=LinearSpacing(2.0),
                           engine=EngineConfig(boxcar_max=1024), baseline_len_s=0.25,
@@ -85,7 +87,7 @@ def test_async_back_halves_match_sync(monkeypatch, initial_cap):
     for sync in (False, True):
         if sync:
             monkeypatch.setenv("PGB_SYNC_BACK", "1")
-        with Engine(0) as eng:
+        with Engine(0, ablations=sync) as eng:  # PGB_SYNC_BACK is an ablation switch
             res.append(eng.search_file(payload, hdr.nsamples, task.chunks, task.plan, task.engine))
     (a, ca, sa), (b, cb, sb) = res
     assert len(a) == len(b) > 0

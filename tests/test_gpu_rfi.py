@@ -9,7 +9,7 @@ import pytest
 
 from paper_2512_00398_b200 import errors
 from paper_2512_00398_b200.dedisp import FilterbankHeader, LinearSpacing, generate_dm_trials
-from paper_2512_00398_b200.engine import EngineConfig, RfiConfig
+from paper_2512_00398_b200.engine import Engine, EngineConfig, RfiConfig
 from paper_2512_00398_b200.pipeline import SearchParams, create_task, read_filterbank, search_file, write_candidates
 
 pytestmark = pytest.mark.gpu
@@ -53,7 +53,8 @@ def test_rfi_scalar_kernels_agree(engine, ref, monkeypatch):
     data = _dirty_u8(5000, 96, seed=11)
     a = engine.rfi_clean(data, _plan(96), RfiConfig())
     monkeypatch.setenv("PGB_RFI_SERIAL", "1")
-    b = engine.rfi_clean(data, _plan(96), RfiConfig())
+    with Engine(0, ablations=True) as abl:
+        b = abl.rfi_clean(data, _plan(96), RfiConfig())
     for x, y in zip(a, b):
         assert np.array_equal(np.asarray(x).view(np.uint8), np.asarray(y).view(np.uint8))
 

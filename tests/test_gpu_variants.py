@@ -1,5 +1,6 @@
-"""Every dedispersion kernel variant the launcher can pick is bit-exact: the env switches
-are read once per process, so each variant runs in its own interpreter on a few of the
+"""Every dedispersion kernel variant is bit-exact: the product library's default choice and
+every PGB_* alternative of the ablation library (libpgb200_ablations.so; the switches are
+read once per process, so each variant runs in its own interpreter) on a few of the
 parity shapes (dedispersed sums against the C restatement of the naive definition)."""
 import os
 import subprocess
@@ -13,7 +14,7 @@ pytestmark = pytest.mark.gpu
 ROOT = Path(__file__).resolve().parents[1]
 
 SNIPPET = r'''
-import sys
+import os, sys
 sys.path.insert(0, {root!r})
 import numpy as np
 from oracle.pyoracle import Port
@@ -23,7 +24,7 @@ from tests.helpers import u8_chunk, f32_chunk
 port = Port()
 cases = [(4096, 1518.0, -0.0703125, 24000, 800.0, 8.0), (1024, 1500.0, -0.25, 20000, 500.0, 2.0),
          (517, 1450.0, -0.5, 12000, 400.0, 2.5)]
-with Engine(0) as eng:
+with Engine(0, ablations=bool(os.environ.get("PG_TEST_ABLATIONS"))) as eng:
     for nch, fch1, foff, L, dm_hi, step in cases:
         hdr = FilterbankHeader(fch1=fch1, foff=foff, nchans=nch, tsamp=64e-6)
         plan = generate_dm_trials(0.0, dm_hi, hdr, LinearSpacing(step))
@@ -51,6 +52,8 @@ print("ok")
 ])
 def test_dedispersion_variants_bit_exact(env):
     e = dict(os.environ, **env)
+    if env:
+        e["PG_TEST_ABLATIONS"] = "1"
     out = subprocess.run([sys.executable, "-c", SNIPPET.format(root=str(ROOT))], env=e,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
@@ -72,6 +75,7 @@ def test_default_selection_covers_both_ring_depths(mode):
     e = dict(os.environ, PGB_DD_WHICH="1")
     if mode:
         e["PGB_RING_MODE"] = mode
+        e["PG_TEST_ABLATIONS"] = "1"
     out = subprocess.run([sys.executable, "-c", WIDE.format(root=str(ROOT))], env=e,
                          capture_output=True, text=True, timeout=600)
     assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
