@@ -264,6 +264,9 @@ pgb_status pgb_launch_count(pgb_context* ctx, uint64_t* launches);
  * and the number of dedispersion launches it covered. */
 pgb_status pgb_last_dedisp_time(pgb_context* ctx, double* ms, uint64_t* launches,
                                 uint64_t* channel_adds);
+/* Host time (ms) of the last file search's file-level sort + link_grid (FileOutcome
+ * cluster_ms, pipeline.hpp:63). */
+pgb_status pgb_last_cluster_ms(pgb_context* ctx, double* ms);
 /* The context's CUDA stream (cudaStream_t), for callers that order their own work. */
 pgb_status pgb_stream(pgb_context* ctx, void** stream);
 /* Measured CUDA-core 32-bit add throughput of `device` (lane-adds/s): the roofline

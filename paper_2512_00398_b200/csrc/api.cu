@@ -182,6 +182,7 @@ struct pgb_context {
     double dedisp_ms = 0.0;
     uint64_t dedisp_launches = 0;
     uint64_t channel_adds = 0;
+    double cluster_ms = 0.0;  // file-level sort + link_grid of the last file search (host clock)
     // last chunk's row geometry for stage fetches
     uint64_t last_out_pitch = 0;
     uint32_t last_nrows = 0;
@@ -917,6 +918,7 @@ void append_chunk_sync(pgb_context* ctx, ChunkRun& run, uint64_t& total) {
 // End of a file: the file-level sort (src/pipeline.cpp:100-105) and link_grid (:106).
 void file_sort_link(pgb_context* ctx, uint64_t total, const pgb_link_radii* radii,
                     size_t* n_candidates, size_t* n_clusters) {
+    const double t0 = host_ms();  // every chunk's work has been synchronised already
     ctx->file_sorted.reserve(std::max<uint64_t>(total, 1) * sizeof(pgb_candidate));
     if (total) {
         const size_t tmp = sort_candidates_temp_bytes(total);
@@ -938,6 +940,7 @@ void file_sort_link(pgb_context* ctx, uint64_t total, const pgb_link_radii* radi
     ctx->n_clusters = ncl;
     ctx->n_members = radii ? total : 0;
     ctx->last_from_file = true;
+    ctx->cluster_ms = host_ms() - t0;
     if (n_candidates) *n_candidates = total;
     if (n_clusters) *n_clusters = ncl;
 }
@@ -1666,6 +1669,13 @@ pgb_status pgb_last_dedisp_time(pgb_context* ctx, double* ms, uint64_t* launches
         if (ms) *ms = ctx->dedisp_ms;
         if (launches) *launches = ctx->dedisp_launches;
         if (adds) *adds = ctx->channel_adds;
+    });
+}
+
+pgb_status pgb_last_cluster_ms(pgb_context* ctx, double* ms) {
+    return guarded([&] {
+        need(ctx && ms, PGB_ERR_ARGUMENT, "null argument");
+        *ms = ctx->cluster_ms;
     });
 }
 

@@ -436,11 +436,17 @@ class Engine:
 
             list(pool.map(rd, range(0, nbytes, step)))
 
+        import time
+
+        t_read = 0.0
+        t0 = time.perf_counter()
         try:
             with ThreadPoolExecutor(1) as reader:
                 fut = reader.submit(fill, 0) if chunks else None
                 for k in range(len(chunks)):
-                    fut.result()
+                    tw = time.perf_counter()
+                    fut.result()  # waiting here = the reader is behind the device
+                    t_read += time.perf_counter() - tw
                     if k + 1 < len(chunks):
                         fut = reader.submit(fill, k + 1)
                     self._check(self._lib.pgb_stream_push(self._h, k, None))
@@ -448,7 +454,16 @@ class Engine:
             pool.shutdown()
         nc, ncl = ctypes.c_size_t(), ctypes.c_size_t()
         self._check(self._lib.pgb_stream_finish(self._h, ctypes.byref(nc), ctypes.byref(ncl)))
+        total = time.perf_counter() - t0
+        cms = ctypes.c_double()
+        self._check(self._lib.pgb_last_cluster_ms(self._h, ctypes.byref(cms)))
+        self._stream_times = {"read_ms": 1e3 * t_read, "cluster_ms": cms.value,
+                              "dm_loop_ms": 1e3 * (total - t_read) - cms.value}
         return self.fetch_file_results(nc.value, ncl.value)
+
+    def last_stream_times(self) -> dict:
+        """Host-clock stage times of the last search_stream (FileOutcome fields)."""
+        return dict(self._stream_times)
 
     def copy_async(self, dst: int, src: int, nbytes: int) -> None:
         """cudaMemcpyAsync on this context's stream (host, device or peer pointers)."""

@@ -117,31 +117,213 @@ def search_file(payload: np.ndarray, task: SearchTask, *, device: int = 0,
     return SearchResult(cands, clusters, skipped)
 
 
-def run_multi_file(payloads: list[np.ndarray], tasks: list[SearchTask], *, n_exec: int = 4,
-                   device: int = 0) -> list[SearchResult | Exception]:
-    """Multi-file execution (src/pipeline.cpp:136-210, next row f3) on one GPU.
+def search_payloads(payloads: list[np.ndarray], tasks: list[SearchTask], *, n_exec: int = 4,
+                    devices: tuple[int, ...] = (0,)) -> list[SearchResult | Exception]:
+    """In-memory multi-file search (config D without disk I/O): `n_exec` host threads, each
+    owning one device context (worker k on devices[k % len(devices)]), take files in
+    submission order; a failing file yields its exception instead of a result."""
+    import queue
+    import threading
 
-    The reference overlaps task creation and execution with two bounded queues of
-    worker threads; here `n_exec` host threads each own a device context (its own
-    CUDA stream and arena, `default_engine` is per thread), so several files'
-    uploads, kernels and syncs interleave on the GPU.  Results are in submission
-    order; a failing file yields its exception instead of a result (per-file
-    isolation, src/pipeline.cpp:173-192)."""
-    from concurrent.futures import ThreadPoolExecutor
+    from .engine import Engine
+    from .errors import ConfigError
 
     if n_exec < 1:
-        from .errors import ConfigError
-
         raise ConfigError("need at least one worker per stage")
+    out: list[SearchResult | Exception | None] = [None] * len(tasks)
+    q: queue.Queue = queue.Queue()
+    for k in range(len(tasks)):
+        q.put(k)
 
-    def one(k):
-        try:
-            return search_file(payloads[k], tasks[k], device=device)
-        except Exception as exc:  # isolate-and-continue
-            return exc
+    def worker(w: int) -> None:
+        with Engine(devices[w % len(devices)]) as eng:
+            while True:
+                try:
+                    k = q.get_nowait()
+                except queue.Empty:
+                    return
+                try:
+                    t = tasks[k]
+                    c, cl, sk = eng.search_file(payloads[k], t.header.nsamples, t.chunks, t.plan, t.engine,
+                                                rfi=t.rfi)
+                    out[k] = SearchResult(c, cl, sk)
+                except Exception as exc:  # isolate-and-continue (src/pipeline.cpp:183-190)
+                    out[k] = exc
 
-    with ThreadPoolExecutor(n_exec) as ex:
-        return list(ex.map(one, range(len(tasks))))
+    threads = [threading.Thread(target=worker, args=(w,)) for w in range(n_exec)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    return out  # type: ignore[return-value]
+
+
+# ---- multi-file pipeline (src/pipeline.cpp:121-219, include/pulsegrid/pipeline.hpp:52-96) ----
+
+@dataclass
+class FileOutcome:
+    """pulsegrid::FileOutcome (pipeline.hpp:52-65): per-file status and stage times (ms)."""
+
+    path: str = ""
+    output_path: str = ""
+    ok: bool = False
+    error: str = ""
+    candidates: int = 0                    # clusters written
+    wall_ms: float = 0.0
+    skipped_trials: list[tuple[int, int]] = field(default_factory=list)  # (chunk, trial)
+    read_ms: float = 0.0                   # waiting for chunk bytes (reader behind compute)
+    rfi_ms: float = 0.0                    # device RFI is inside dm_loop_ms (one stream)
+    dm_loop_ms: float = 0.0
+    cluster_ms: float = 0.0
+    write_ms: float = 0.0
+    device: int = 0
+
+
+@dataclass
+class RunSummary:
+    """pulsegrid::RunSummary (pipeline.hpp:67-71)."""
+
+    files: list[FileOutcome]
+    total_wall_ms: float = 0.0
+    n_failed: int = 0
+
+
+def assign_output_paths(paths: list[str], output_dir: str) -> list[str]:
+    """src/pipeline.cpp:121-133: <output_dir>/<stem>.cand, repeated stems numbered."""
+    seen: dict[str, int] = {}
+    out = []
+    for p in paths:
+        stem = Path(p).stem or "output"
+        seen[stem] = seen.get(stem, 0) + 1
+        n = seen[stem]
+        out.append(str(Path(output_dir) / (f"{stem}.cand" if n == 1 else f"{stem}.{n}.cand")))
+    return out
+
+
+@dataclass
+class PipelineTask:
+    """pulsegrid::PipelineTask (pipeline.hpp:41-50)."""
+
+    index: int
+    path: str
+    output_path: str
+    task: SearchTask
+    data_offset: int
+
+
+def create_file_task(path: str, params: SearchParams, output_path: str, index: int = 0) -> PipelineTask:
+    """create_task on a file (src/pipeline.cpp:32-59): header, DM plan, chunk plan."""
+    from .errors import PulsegridError
+
+    hdr, off = read_filterbank_header(path)
+    if hdr.nsamples == 0:
+        raise PulsegridError(f"'{path}' has no samples")
+    return PipelineTask(index, str(path), output_path, create_task(hdr, params), off)
+
+
+def execute_task(pt: PipelineTask, eng, read_threads: int = 4) -> FileOutcome:
+    """execute_task (src/pipeline.cpp:61-119) on the device: streamed chunks (bounded memory),
+    the chunk chain, file sort + link_grid, one .cand file; stage times in the outcome."""
+    import os
+    import time
+
+    t0 = time.perf_counter()
+    out = FileOutcome(path=pt.path, output_path=pt.output_path, device=eng.device)
+    fd = os.open(pt.path, os.O_RDONLY)
+    try:
+        t = pt.task
+        c, cl, sk = eng.search_stream(fd, pt.data_offset, t.header.nsamples, t.chunks, t.plan, t.engine,
+                                      rfi=t.rfi, read_threads=read_threads)
+    finally:
+        os.close(fd)
+    st = eng.last_stream_times()
+    out.read_ms, out.dm_loop_ms, out.cluster_ms = st["read_ms"], st["dm_loop_ms"], st["cluster_ms"]
+    tw = time.perf_counter()
+    text = write_candidates(cl)
+    with open(pt.output_path, "w") as f:
+        f.write(text)
+    out.write_ms = 1e3 * (time.perf_counter() - tw)
+    out.candidates = len(cl)
+    out.skipped_trials = [(int(a), int(b)) for a, b in np.asarray(sk).reshape(-1, 2)]
+    out.ok = True
+    out.wall_ms = 1e3 * (time.perf_counter() - t0)
+    return out
+
+
+def run_multi_file(paths: list[str], params: SearchParams, output_dir: str, n_create: int = 1,
+                   n_exec: int = 2, creation_capacity: int = 0, execution_capacity: int = 0, *,
+                   devices: tuple[int, ...] = (0,), read_threads: int = 4) -> RunSummary:
+    """Two-stage multi-file pipeline (src/pipeline.cpp:136-210): n_create workers parse
+    headers and build plans, n_exec workers execute them through bounded queues (capacity
+    2x the stage's workers by default), per-file failures isolated into the summary.  Each
+    execution worker owns one device context; worker k runs on devices[k % len(devices)],
+    so a batch spreads over the node's GPUs.  The memory budget is split across the
+    execution workers like the reference's (:163-166)."""
+    import queue
+    import threading
+    import time
+
+    from .engine import Engine
+    from .errors import ConfigError
+
+    if n_create < 1 or n_exec < 1:
+        raise ConfigError("need at least one worker per stage")
+    t0 = time.perf_counter()
+    Path(output_dir).mkdir(parents=True, exist_ok=True)
+    outs = assign_output_paths([str(p) for p in paths], output_dir)
+    summary = RunSummary([FileOutcome(path=str(p), output_path=o) for p, o in zip(paths, outs)])
+    wp = SearchParams(**{k: getattr(params, k) for k in params.__dataclass_fields__})
+    wp.engine = EngineConfig(**{k: getattr(params.engine, k) for k in params.engine.__dataclass_fields__})
+    wp.engine.memory_budget = max(1, params.engine.memory_budget // n_exec)
+    cq: queue.Queue = queue.Queue(creation_capacity or 2 * n_create)
+    eq: queue.Queue = queue.Queue(execution_capacity or 2 * n_exec)
+    STOP = object()
+
+    def creator():
+        while (item := cq.get()) is not STOP:
+            try:
+                eq.put(create_file_task(str(paths[item]), wp, outs[item], item))
+            except Exception as exc:
+                summary.files[item].ok = False
+                summary.files[item].error = str(exc)
+
+    def executor(w: int):
+        with Engine(devices[w % len(devices)]) as eng:
+            while (pt := eq.get()) is not STOP:
+                try:
+                    summary.files[pt.index] = execute_task(pt, eng, read_threads)
+                except Exception as exc:
+                    summary.files[pt.index].ok = False
+                    summary.files[pt.index].error = str(exc)
+
+    creators = [threading.Thread(target=creator) for _ in range(n_create)]
+    executors = [threading.Thread(target=executor, args=(w,)) for w in range(n_exec)]
+    for t in creators + executors:
+        t.start()
+    for i in range(len(paths)):
+        cq.put(i)
+    for _ in creators:
+        cq.put(STOP)
+    for t in creators:
+        t.join()
+    for _ in executors:  # creators done: drain and stop the executors
+        eq.put(STOP)
+    for t in executors:
+        t.join()
+    summary.n_failed = sum(not f.ok for f in summary.files)
+    summary.total_wall_ms = 1e3 * (time.perf_counter() - t0)
+    return summary
+
+
+def write_summary(summary: RunSummary) -> str:
+    """src/pipeline.cpp:212-219: path, status, candidate count, wall ms (+ error)."""
+    lines = []
+    for f in summary.files:
+        line = f"{f.path}\t{'ok' if f.ok else 'error'}\t{f.candidates}\t{int(round(f.wall_ms))}"
+        if not f.ok:
+            line += f"\t{f.error}"
+        lines.append(line + "\n")
+    return "".join(lines)
 
 
 def write_candidates(clusters: Clusters) -> str:

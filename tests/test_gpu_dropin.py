@@ -81,3 +81,24 @@ def test_link_substitution_f32_file(ref, tmp_path):
     assert a["chunks"] > 1
     assert (tmp_path / "b200.cand").read_text() == (tmp_path / "ref.cand").read_text()
     assert a["clusters"] == b["clusters"] > 0
+
+
+@pytest.mark.slow
+def test_link_substitution_config_b_matches_golden(tmp_path):
+    """The reference's own execute_task with our engine/cluster TUs linked in, on the full
+    config-B file (5 chunks of read_chunk's widened floats, repacked to bytes on the host
+    before the upload): .cand bytes equal the pure reference's (tests/golden/config_B.npz)."""
+    import numpy as np
+
+    from tests.helpers import task_for
+    from tools import synth
+
+    _need_binaries()
+    z = np.load(Path(__file__).resolve().parent / "golden" / "config_B.npz")
+    cfg = json.loads(str(z["meta"]))["cfg"]
+    fil = tmp_path / "B.fil"
+    synth.write_filterbank(fil, cfg, task_for(cfg).plan.delays)
+    args = (cfg["dm_lo"], cfg["dm_hi"], cfg["dm_step"], cfg["boxcar_max"], cfg["baseline_s"], cfg["nsamps_chunk"], 16)
+    b = _run("pipeline_b200", fil, tmp_path / "b200.cand", args)
+    assert b["chunks"] == 5
+    assert (tmp_path / "b200.cand").read_text() == z["cand_text"].tobytes().decode()

@@ -38,6 +38,7 @@ def run_file(cfg, steps, label=None):
     dd = 0.0
     adds = 0
     torch.cuda.synchronize()
+    clk = bench.ClockSampler(0).__enter__()
     t0 = time.perf_counter()
     for _ in range(steps):
         cands, clusters, _ = eng.search_file(payload, cfg["nsamples"], task.chunks, task.plan, task.engine,
@@ -47,40 +48,68 @@ def run_file(cfg, steps, label=None):
         adds += a
     torch.cuda.synchronize()
     el = (time.perf_counter() - t0) / steps
+    clk.__exit__(None, None, None)
     units = task.plan.ntrials * cfg["nsamples"]
     return {"config": label or cfg["workload"], "ntrials": task.plan.ntrials, "nchans": cfg["nchans"],
             "nsamples": cfg["nsamples"], "chunks": len(task.chunks), "rfi": bool(cfg.get("rfi")),
             "value": units / el, "unit": "DM-trial*samples/s", "x_realtime": cfg["nsamples"] * cfg["tsamp"] / el,
             "s_per_file": el, "dedisp_tadd_s": adds / (dd / 1e3) / 1e12 if dd else None,
             "dedisp_share": (dd / steps / 1e3) / el, "candidates": int(len(cands)),
-            "clusters": int(len(clusters)), "timing": "host wall clock around synchronous file searches"}
+            "clusters": int(len(clusters)), "clocks": clk.summary(),
+            "timing": "host wall clock around synchronous file searches (payload resident)"}
 
 
 def run_multi(steps, nfiles=32, n_exec=4):
-    """Config D: 32 config-A files, n_exec device contexts (one stream each) working concurrently."""
+    """Config D: 32 config-A files (seeds 2000+i) held in host memory, n_exec device contexts
+    (one stream each) taking files concurrently (pipeline.search_payloads)."""
+    from paper_2512_00398_b200.pipeline import search_payloads
+
     cfg = dict(CONFIGS["A"])
     task = bench.build_task(cfg)
-    payloads = []
-    for i in range(nfiles):
-        c = dict(cfg, seed=2000 + i)
-        payloads.append(bench.make_payload(c, task.plan))
-    torch.cuda.synchronize()
-
-    def one(i):
-        eng = default_engine(0)
-        cands, clusters, _ = eng.search_file(payloads[i], cfg["nsamples"], task.chunks, task.plan, task.engine)
-        return len(clusters)
-
-    with ThreadPoolExecutor(n_exec) as ex:
-        list(ex.map(one, range(nfiles)))  # warm-up (creates the per-thread contexts)
+    payloads = [synth.payload(dict(cfg, seed=2000 + i), task.plan.delays) for i in range(nfiles)]
+    search_payloads(payloads, [task] * nfiles, n_exec=n_exec)  # warm-up
+    with bench.ClockSampler(0) as clk:
         t0 = time.perf_counter()
         for _ in range(steps):
-            list(ex.map(one, range(nfiles)))
+            res = search_payloads(payloads, [task] * nfiles, n_exec=n_exec)
         el = (time.perf_counter() - t0) / steps
+    assert not any(isinstance(r, Exception) for r in res)
     units = nfiles * task.plan.ntrials * cfg["nsamples"]
     return {"config": "config_D_32xA", "files": nfiles, "n_exec": n_exec, "value": units / el,
             "unit": "DM-trial*samples/s", "x_realtime": nfiles * cfg["nsamples"] * cfg["tsamp"] / el,
-            "s_per_batch": el, "timing": "host wall clock around the concurrent batch"}
+            "s_per_batch": el, "clocks": clk.summary(),
+            "timing": "host wall clock around the concurrent batch (host payloads, H2D included)"}
+
+
+def run_multi_disk(steps, nfiles=32, n_exec=4, workdir="/tmp/pg_configD"):
+    """Config D from disk: the 32 files written as 8-bit SIGPROC files, run_multi_file
+    (2 creation + n_exec execution workers, streamed chunks, .cand files written)."""
+    from paper_2512_00398_b200.pipeline import run_multi_file
+    from tests.test_gpu_stream import _params
+
+    cfg = dict(CONFIGS["A"])
+    task = bench.build_task(cfg)
+    Path(workdir).mkdir(parents=True, exist_ok=True)
+    paths = []
+    for i in range(nfiles):
+        p = Path(workdir) / f"A{i:02d}.fil"
+        synth.write_filterbank(p, dict(cfg, seed=2000 + i), task.plan.delays)
+        paths.append(str(p))
+    params = _params(cfg)
+    run_multi_file(paths, params, workdir + "/out", n_create=2, n_exec=n_exec)  # warm-up (page cache)
+    with bench.ClockSampler(0) as clk:
+        t0 = time.perf_counter()
+        for _ in range(steps):
+            s = run_multi_file(paths, params, workdir + "/out", n_create=2, n_exec=n_exec)
+        el = (time.perf_counter() - t0) / steps
+    assert s.n_failed == 0
+    units = nfiles * task.plan.ntrials * cfg["nsamples"]
+    return {"config": "config_D_32xA_from_disk", "files": nfiles, "n_exec": n_exec, "value": units / el,
+            "unit": "DM-trial*samples/s", "x_realtime": nfiles * cfg["nsamples"] * cfg["tsamp"] / el,
+            "s_per_batch": el, "clocks": clk.summary(),
+            "stage_ms_mean": {k: float(np.mean([getattr(f, k) for f in s.files]))
+                              for k in ("read_ms", "dm_loop_ms", "cluster_ms", "write_ms", "wall_ms")},
+            "timing": "host wall clock around run_multi_file (files in page cache)"}
 
 
 def main():
@@ -92,6 +121,8 @@ def main():
     for name in args.configs:
         if name == "D":
             out = run_multi(args.steps, n_exec=args.n_exec)
+        elif name == "Ddisk":
+            out = run_multi_disk(args.steps, n_exec=args.n_exec)
         else:
             out = run_file(dict(CONFIGS[name]), args.steps)
         print(json.dumps(out), flush=True)
