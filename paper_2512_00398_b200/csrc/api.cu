@@ -365,6 +365,7 @@ namespace {
 
 void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spec,
                  const pgb_engine_config* cfg, int slot, ChunkRun& run) {
+    NvtxRange nvtx("pgb chunk front (transpose, dedispersion, baseline, rms)");
     cudaStream_t st = ctx->st;
     const uint64_t L = spec->length;
     const uint32_t C = ctx->nchans;
@@ -425,6 +426,9 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     std::vector<uint32_t> blk_len(nblocks, 0);
     for (uint32_t r = 0; r < nrows; ++r) blk_len[r / tb] = std::max(blk_len[r / tb], row_len[r]);
     const bool u8 = in.u8;
+    if (u8 && C > PGB_MAX_EXACT_CHANS)
+        raise(PGB_ERR_CONFIG, "8-bit input with more than 65793 channels: the integer channel sums pass "
+                              "2^24, where the reference's fp32 sums start rounding (widen to floats)");
     // Blocks whose channel delay spread fits a staged window go through the shared-memory
     // kernels; wider ones (very coarse DM steps) through the direct kernel, which reads
     // the channel rows from L1/L2.  The staged kernels skip those (block length 0).
@@ -728,6 +732,7 @@ double* box_levels(pgb_context* ctx, uint64_t boxcar_max, uint32_t nrows, uint64
 }
 
 void chunk_back(pgb_context* ctx, ChunkRun& run) {
+    NvtxRange nvtx("pgb chunk back (boxcar, runs, order)");
     cudaStream_t st = ctx->st;
     const int slot = run.slot;
     const pgb_chunk_spec* spec = &run.spec;
@@ -837,6 +842,7 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
 // degenerate-trial flags copied to pinned host memory.  The file search reads all of it
 // once at the end and re-runs the file with larger capacities if a counter overflowed.
 void chunk_back_async(pgb_context* ctx, ChunkRun& run, uint8_t* h_status, uint64_t file_cap) {
+    NvtxRange nvtx("pgb chunk back (async)");
     cudaStream_t st = ctx->st;
     const int slot = run.slot;
     if (!run.live) return;
@@ -918,6 +924,7 @@ void append_chunk_sync(pgb_context* ctx, ChunkRun& run, uint64_t& total) {
 // End of a file: the file-level sort (src/pipeline.cpp:100-105) and link_grid (:106).
 void file_sort_link(pgb_context* ctx, uint64_t total, const pgb_link_radii* radii,
                     size_t* n_candidates, size_t* n_clusters) {
+    NvtxRange nvtx("pgb file sort + link_grid");
     const double t0 = host_ms();  // every chunk's work has been synchronised already
     ctx->file_sorted.reserve(std::max<uint64_t>(total, 1) * sizeof(pgb_candidate));
     if (total) {
@@ -958,7 +965,8 @@ void run_chunk(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* spe
 // path: every in-order fp32 partial sum is then an exact integer, so series and
 // baselines are bit-identical.  Repacked on the device; otherwise the fp32 path.
 ChunkInput prepare_f32(pgb_context* ctx, const float* dptr, uint64_t length) {
-    if (!ctx->ntrials || !length || pgb_ablation_env("PGB_FORCE_F32_PATH")) return ChunkInput{dptr, false};
+    if (!ctx->ntrials || !length || ctx->nchans > PGB_MAX_EXACT_CHANS || pgb_ablation_env("PGB_FORCE_F32_PATH"))
+        return ChunkInput{dptr, false};
     const size_t cells = (size_t)length * ctx->nchans;
     ctx->in_u8.reserve(cells);
     ctx->counters.reserve(4 * sizeof(unsigned long long));
@@ -1219,6 +1227,7 @@ static pgb_status run_dm_loop_impl(pgb_context* ctx, const void* data, bool u8, 
                                    const pgb_chunk_spec* spec, const pgb_engine_config* cfg,
                                    size_t* n_candidates, size_t* n_skipped) {
     return guarded([&] {
+        NvtxRange nvtx("pgb run_dm_loop");
         need(ctx && data, PGB_ERR_ARGUMENT, "null ctx/data");
         PGB_CUDA(cudaSetDevice(ctx->device));
         validate_cfg(ctx, spec, cfg);
@@ -1229,7 +1238,7 @@ static pgb_status run_dm_loop_impl(pgb_context* ctx, const void* data, bool u8, 
         const size_t bytes = cells * (u8 ? 1 : 4);
         bool as_u8 = u8;
         if (!on_device && ctx->ntrials) {
-            if (!u8) {
+            if (!u8 && ctx->nchans <= PGB_MAX_EXACT_CHANS) {
                 // read_chunk widens 8-bit files to floats (src/filterbank.cpp:304-307): repack
                 // integer chunks to bytes on the host threads, so a quarter of the bytes cross
                 // PCIe from pinned memory; any non-integer cell keeps the fp32 upload
@@ -1362,6 +1371,7 @@ pgb_status pgb_rfi_clean(pgb_context* ctx, const void* data, int is_u8, int on_d
                          uint64_t length, const pgb_rfi_config* rfi, float* out_host,
                          uint64_t* n_bad_channels, uint64_t* n_bad_samples) {
     return guarded([&] {
+        NvtxRange nvtx("pgb rfi_clean");
         need(ctx && data && rfi && ctx->nchans, PGB_ERR_ARGUMENT, "null argument or no plan");
         PGB_CUDA(cudaSetDevice(ctx->device));
         const uint32_t C = ctx->nchans;
@@ -1404,6 +1414,7 @@ pgb_status pgb_fetch_rfi_flags(pgb_context* ctx, uint8_t* bad_channels, uint8_t*
 pgb_status pgb_link_grid(pgb_context* ctx, const pgb_candidate* cands, int on_device, size_t n,
                          const pgb_link_radii* radii, size_t* n_clusters) {
     return guarded([&] {
+        NvtxRange nvtx("pgb link_grid");
         need(ctx && radii && (n == 0 || cands), PGB_ERR_ARGUMENT, "null argument");
         PGB_CUDA(cudaSetDevice(ctx->device));
         const pgb_candidate* dptr = cands;
@@ -1445,6 +1456,7 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                               const pgb_engine_config* cfg, const pgb_link_radii* radii,
                               const pgb_rfi_config* rfi, size_t* n_candidates, size_t* n_clusters) {
     return guarded([&] {
+        NvtxRange nvtx("pgb search_file_u8");
         need(ctx && payload && cfg && (nchunks == 0 || chunks), PGB_ERR_ARGUMENT,
              "null argument");
         PGB_CUDA(cudaSetDevice(ctx->device));
@@ -1765,6 +1777,7 @@ pgb_status pgb_stream_buffer(pgb_context* ctx, size_t k, uint8_t** host_buffer, 
 
 pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
     return guarded([&] {
+        NvtxRange nvtx("pgb stream push");
         need(ctx, PGB_ERR_ARGUMENT, "null ctx");
         auto& S = ctx->stream;
         need(S.open && k == S.next && k < S.chunks.size(), PGB_ERR_ARGUMENT, "chunks are pushed in order");

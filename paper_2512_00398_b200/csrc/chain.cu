@@ -24,7 +24,11 @@
 #include <cmath>
 #include <utility>
 
+#include <cooperative_groups.h>
+
 #include "pgb_internal.h"
+
+namespace cg = cooperative_groups;
 
 namespace pgb {
 
@@ -675,6 +679,16 @@ struct PeakCtx {
     uint64_t frag_cap;
 };
 
+// Warp-aggregated append: the lanes emitting together take consecutive slots with one
+// atomicAdd by the first of them (the buffer is sorted by a unique key afterwards, so the
+// slot order does not matter).
+__device__ __forceinline__ unsigned long long warp_slot(unsigned long long* counter) {
+    const cg::coalesced_group g = cg::coalesced_threads();
+    unsigned long long base = 0;
+    if (g.thread_rank() == 0) base = atomicAdd(counter, (unsigned long long)g.size());
+    return g.shfl(base, 0) + g.thread_rank();
+}
+
 __device__ void emit_candidate(const PeakCtx& c, uint32_t row, uint32_t level, uint64_t m,
                                uint64_t b, uint64_t e, uint64_t pk, double pv) {
     const ChainParams& cp = c.cp;
@@ -682,7 +696,7 @@ __device__ void emit_candidate(const PeakCtx& c, uint32_t row, uint32_t level, u
     if (cp.drop_right && e == m - 1) return;      // :236
     const uint64_t abs_peak = cp.start_sample + pk;
     if (abs_peak < cp.valid_begin || abs_peak >= cp.valid_end) return;  // :237-238
-    const unsigned long long slot = atomicAdd(c.n_cands, 1ull);
+    const unsigned long long slot = warp_slot(c.n_cands);
     if (slot >= c.cand_cap) return;
     pgb_candidate out;
     out.snr = __double2float_rn(pv);
@@ -703,7 +717,7 @@ __device__ void emit_candidate(const PeakCtx& c, uint32_t row, uint32_t level, u
 
 __device__ void emit_fragment(const PeakCtx& c, uint32_t row, uint32_t level, uint64_t b,
                               uint64_t e, uint64_t pk, double pv) {
-    const unsigned long long slot = atomicAdd(c.n_frags, 1ull);
+    const unsigned long long slot = warp_slot(c.n_frags);
     if (slot >= c.frag_cap) return;
     Fragment f;
     f.key = (uint64_t)row << 40 | (uint64_t)level << 35 | b;

@@ -47,13 +47,25 @@ __device__ __forceinline__ uint64_t cell_key(uint64_t kt, uint64_t kd, uint64_t 
     return kt << 24 | kd << 5 | kw;
 }
 
+// Largest width (cell extent) and the key-packing limits every later stage relies on:
+// dm_trial < 2^20, width_index < 32, peak_sample < 2^39 (sort keys peak<<25|trial<<5|width
+// and peak<<20|trial); bad != 0 makes pgb_link_grid fail with PGB_ERR_ARGUMENT.
 __global__ void wmax_kernel(const pgb_candidate* __restrict__ c, uint64_t n,
-                            unsigned long long* wmax) {
+                            unsigned long long* wmax, unsigned long long* bad) {
     const uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x;
     uint64_t w = 1;
-    if (i < n) w = c[i].width_samples;
+    unsigned long long out = 0;
+    if (i < n) {
+        const pgb_candidate a = c[i];
+        w = a.width_samples;
+        out = (a.dm_trial >= (1u << 20)) | (a.width_index >= 32u) | (a.peak_sample >= (1ull << 39));
+    }
     for (int o = 16; o; o >>= 1) w = max(w, (uint64_t)__shfl_xor_sync(0xffffffffu, w, o));
-    if ((threadIdx.x & 31) == 0) atomicMax(wmax, (unsigned long long)w);
+    out = __any_sync(0xffffffffu, out != 0);
+    if ((threadIdx.x & 31) == 0) {
+        atomicMax(wmax, (unsigned long long)w);
+        if (out) atomicOr(bad, 1ull);
+    }
 }
 
 struct CellGeom {
@@ -438,7 +450,7 @@ void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_r
                         uint64_t* nclusters, cudaStream_t st, uint64_t* launches) {
     *nclusters = 0;
     if (n == 0) return;
-    if (n >= (1ull << 32) - 1) raise(PGB_ERR_ARGUMENT, "too many candidates to cluster");
+    if (n >= (1ull << 31)) raise(PGB_ERR_ARGUMENT, "too many candidates to cluster (>= 2^31)");
     size_t sort_tmp = 0;
     {
         cub::DoubleBuffer<uint64_t> k(nullptr, nullptr);
@@ -455,8 +467,9 @@ void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_r
     out_members.reserve(n * sizeof(uint64_t));
 
     char* p = scratch.as<char>();
-    auto* wmax = carve<unsigned long long>(p, 2);
+    auto* wmax = carve<unsigned long long>(p, 3);
     auto* ncl = wmax + 1;
+    auto* bad = wmax + 2;
     auto* keys_a = carve<uint64_t>(p, n);
     auto* keys_b = carve<uint64_t>(p, n);
     auto* rkeys_a = carve<uint64_t>(p, n);
@@ -480,8 +493,8 @@ void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_r
     void* cub_tmp = carve<char>(p, sort_tmp);
 
     const Radii r{radii.sep_time, radii.sep_dm_trials, radii.sep_width};
-    PGB_CUDA(cudaMemsetAsync(wmax, 0, 2 * sizeof(unsigned long long), st));
-    wmax_kernel<<<nblk(n), 256, 0, st>>>(cands, n, wmax);
+    PGB_CUDA(cudaMemsetAsync(wmax, 0, 3 * sizeof(unsigned long long), st));
+    wmax_kernel<<<nblk(n), 256, 0, st>>>(cands, n, wmax, bad);
     const CellGeom g{wmax, r};
     init_kernel<<<nblk(n), 256, 0, st>>>(cands, n, g, keys_a, idx_a, rkeys_a, ridx_a, parent,
                                          repkey, cnt, bmin, emax, dlo, dhi);
@@ -529,9 +542,13 @@ void cluster_candidates(const pgb_candidate* cands, uint64_t n, const pgb_link_r
                                                    bmin, emax, dlo, dhi, member_start, cl_tmp,
                                                    keys_a, idx_a);
     PGB_CUDA(cudaGetLastError());
-    unsigned long long h_ncl = 0;
-    PGB_CUDA(cudaMemcpyAsync(&h_ncl, ncl, sizeof h_ncl, cudaMemcpyDeviceToHost, st));
+    unsigned long long h_cnt[2] = {0, 0};  // ncl, bad
+    PGB_CUDA(cudaMemcpyAsync(h_cnt, ncl, sizeof h_cnt, cudaMemcpyDeviceToHost, st));
     PGB_CUDA(cudaStreamSynchronize(st));
+    if (h_cnt[1])
+        raise(PGB_ERR_ARGUMENT, "link_grid: candidate fields beyond the device key packing "
+                                "(dm_trial < 2^20, width_index < 32, peak_sample < 2^39)");
+    const unsigned long long h_ncl = h_cnt[0];
     *nclusters = h_ncl;
     cub::DoubleBuffer<uint64_t> sk(keys_a, keys_b);
     cub::DoubleBuffer<uint32_t> sv(idx_a, idx_b);

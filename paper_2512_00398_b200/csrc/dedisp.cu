@@ -285,6 +285,9 @@ __device__ __forceinline__ uint32_t sh_addr(const void* p) {
 __device__ __forceinline__ void ring_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sh_addr(bar)), "r"(count) : "memory");
 }
+__device__ __forceinline__ void ring_inval(uint64_t* bar) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(sh_addr(bar)) : "memory");
+}
 __device__ __forceinline__ void ring_arrive(uint64_t* bar) {
     asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(sh_addr(bar)) : "memory");
 }
@@ -550,6 +553,15 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
         ph_prev = ph;
         if (++slot == NS) { slot = 0; ph ^= 1; }
         if (++slot2 == NS) slot2 = 0;
+    }
+    // the barriers are re-initialised for the next (block, tile) item: invalidate them
+    // once every warp is past its last wait on them
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < NS; ++s) {
+            ring_inval(full + s);
+            ring_inval(empty + s);
+        }
     }
 }
 

@@ -15,6 +15,17 @@
 // can change its code path.  Diagnostics (PGB_TRACE, PGB_DD_WHICH) and the initial
 // buffer capacity (PGB_INITIAL_CAP, never changes results) are read by both.
 #include <cstdlib>
+// NVTX ranges around the host-side stages (header-only NVTX v3): a profiler timeline
+// (nsys / ncu --nvtx) shows "pgb ..." ranges for the chunk front and back halves, the
+// file-level sort + link_grid, RFI excision and the streaming pushes.
+#include <nvtx3/nvToolsExt.h>
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
+
 inline const char* pgb_ablation_env(const char* name) {
 #ifdef PGB_ABLATIONS
     return std::getenv(name);
@@ -67,6 +78,9 @@ constexpr int DD_WORDS = DD_NT / 128;   // u8 path: 4-byte words per lane per tr
 constexpr int DD_FOUT = DD_NT / 32;     // f32 path: outputs per lane per trial (32)
 constexpr int DD_FLUSH_CH = 256;        // u16-lane SWAR accumulators flush period (channels)
 constexpr size_t DD_SMEM_BUDGET = 200 * 1024;
+// Integer (8-bit) dedispersion equals the reference's in-order fp32 sums while every
+// partial sum is an exact float integer: nchans * 255 < 2^24, i.e. nchans <= 65793.
+constexpr uint32_t PGB_MAX_EXACT_CHANS = 65793;
 
 // Boxcar/peak CTA: buffer of BX_N doubles, BX_THREADS threads.
 constexpr int BX_THREADS = 512;

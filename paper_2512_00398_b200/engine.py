@@ -534,6 +534,25 @@ def default_engine(device: int = 0) -> Engine:
         return eng
 
 
+_idle: dict[int, list[Engine]] = {}
+
+
+def acquire_engine(device: int = 0) -> Engine:
+    """An idle device context from the process-wide pool (created on first use).  The
+    multi-file workers take one per file batch and hand it back, so contexts, streams and
+    their grown device arenas outlive a batch instead of paying cudaMalloc per call."""
+    with _lock:
+        free = _idle.setdefault(device, [])
+        if free:
+            return free.pop()
+    return Engine(device)
+
+
+def release_engine(eng: Engine) -> None:
+    with _lock:
+        _idle.setdefault(eng.device, []).append(eng)
+
+
 def run_dm_loop(chunk: Chunk, plan: DmTrialPlan, cfg: EngineConfig, pool=None, *,
                 device: int = 0) -> DmLoopResult:
     """pulsegrid::run_dm_loop (engine.hpp:61-62) on the B200."""

@@ -125,7 +125,7 @@ def search_payloads(payloads: list[np.ndarray], tasks: list[SearchTask], *, n_ex
     import queue
     import threading
 
-    from .engine import Engine
+    from .engine import acquire_engine, release_engine
     from .errors import ConfigError
 
     if n_exec < 1:
@@ -136,7 +136,8 @@ def search_payloads(payloads: list[np.ndarray], tasks: list[SearchTask], *, n_ex
         q.put(k)
 
     def worker(w: int) -> None:
-        with Engine(devices[w % len(devices)]) as eng:
+        eng = acquire_engine(devices[w % len(devices)])
+        try:
             while True:
                 try:
                     k = q.get_nowait()
@@ -149,6 +150,8 @@ def search_payloads(payloads: list[np.ndarray], tasks: list[SearchTask], *, n_ex
                     out[k] = SearchResult(c, cl, sk)
                 except Exception as exc:  # isolate-and-continue (src/pipeline.cpp:183-190)
                     out[k] = exc
+        finally:
+            release_engine(eng)
 
     threads = [threading.Thread(target=worker, args=(w,)) for w in range(n_exec)]
     for t in threads:
@@ -263,7 +266,7 @@ def run_multi_file(paths: list[str], params: SearchParams, output_dir: str, n_cr
     import threading
     import time
 
-    from .engine import Engine
+    from .engine import acquire_engine, release_engine
     from .errors import ConfigError
 
     if n_create < 1 or n_exec < 1:
@@ -288,13 +291,16 @@ def run_multi_file(paths: list[str], params: SearchParams, output_dir: str, n_cr
                 summary.files[item].error = str(exc)
 
     def executor(w: int):
-        with Engine(devices[w % len(devices)]) as eng:
+        eng = acquire_engine(devices[w % len(devices)])
+        try:
             while (pt := eq.get()) is not STOP:
                 try:
                     summary.files[pt.index] = execute_task(pt, eng, read_threads)
                 except Exception as exc:
                     summary.files[pt.index].ok = False
                     summary.files[pt.index].error = str(exc)
+        finally:
+            release_engine(eng)
 
     creators = [threading.Thread(target=creator) for _ in range(n_create)]
     executors = [threading.Thread(target=executor, args=(w,)) for w in range(n_exec)]

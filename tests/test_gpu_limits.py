@@ -128,13 +128,14 @@ def test_boxcar_max_above_tile_ladder_interior_chunk(engine, ref):
     hdr = FilterbankHeader(fch1=1500.0, foff=-0.25, nchans=1024, tsamp=64e-6)
     plan = generate_dm_trials(0.0, 120.0, hdr, LinearSpacing(4.0))
     L = 1 << 17
-    data = _payload(hdr, plan, L, 809, [(7, 1000, 16384, 80.0), (9, 70000, 8192, 70.0),
-                                        (3, L - 20000, 16384, 80.0)])
+    # (amplitudes above half a code: smaller ones vanish in the round-half-up quantisation)
+    data = _payload(hdr, plan, L, 809, [(7, 1000, 16384, 500.0), (9, 70000, 8192, 350.0),
+                                        (3, L - 20000, 16384, 500.0)])
     spec = ChunkSpec(index=2, start_sample=300000, length=L, overlap=20000, valid_begin=300000,
                      valid_end=300000 + L - 20000)
-    cfg = EngineConfig(n_workers=16, tsamp=hdr.tsamp, boxcar_max=16384, baseline_window=0)
+    cfg = EngineConfig(n_workers=16, tsamp=hdr.tsamp, boxcar_max=16384, baseline_window=65537)
     res = engine.run_dm_loop(Chunk(spec, data), plan, cfg)
     want, want_sk, _ = ref.run_dm_loop(data, vars(spec), plan.dms, plan.delays, cfg_dict(cfg))
-    assert len(want) > 0
+    assert (want["width_index"] >= 13).any()
     assert_same_candidates(res.candidates, want)
     assert np.array_equal(res.skipped_trials, want_sk)
