@@ -66,7 +66,9 @@ def run_multi(steps, nfiles=32, n_exec=4):
 
     cfg = dict(CONFIGS["A"])
     task = bench.build_task(cfg)
-    payloads = [synth.payload(dict(cfg, seed=2000 + i), task.plan.delays) for i in range(nfiles)]
+    # host payloads in pinned memory (a reader would fill pinned buffers, as search_fil does)
+    payloads = [torch.from_numpy(synth.payload(dict(cfg, seed=2000 + i), task.plan.delays)).pin_memory().numpy()
+                for i in range(nfiles)]
     search_payloads(payloads, [task] * nfiles, n_exec=n_exec)  # warm-up
     with bench.ClockSampler(0) as clk:
         t0 = time.perf_counter()
