@@ -264,6 +264,12 @@ pgb_status pgb_launch_count(pgb_context* ctx, uint64_t* launches);
  * and the number of dedispersion launches it covered. */
 pgb_status pgb_last_dedisp_time(pgb_context* ctx, double* ms, uint64_t* launches,
                                 uint64_t* channel_adds);
+/* Device time (ms) of each stage of the last pgb_run_dm_loop_* call, measured with CUDA
+ * events: ms[0] dedispersion, [1] baseline removal, [2] normalisation (robust RMS),
+ * [3] boxcar ladder with the threshold runs, [4] run stitching + candidate order.  The
+ * stages run batched over every trial of the chunk; the C++ drop-in amortises them over
+ * the processed trials for TrialTiming (engine.hpp:16-23). */
+pgb_status pgb_last_stage_times(pgb_context* ctx, double* ms /* [5] */);
 /* Host time (ms) of the last file search's file-level sort + link_grid (FileOutcome
  * cluster_ms, pipeline.hpp:63). */
 pgb_status pgb_last_cluster_ms(pgb_context* ctx, double* ms);

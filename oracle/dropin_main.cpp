@@ -10,8 +10,12 @@
 // the files byte for byte.
 //
 // usage: pipeline_* in.fil out.cand dm_lo dm_hi dm_step boxcar_max baseline_s nsamps_chunk n_workers [rfi]
+// PG_TIMING_OUT=path: EngineConfig::timing_sink appends one line per TrialTiming record
+// ("trial dedisperse baseline normalize boxcar peaks", ms) to path.
 #include <cstdio>
 #include <cstdlib>
+#include <mutex>
+#include <stdexcept>
 #include <string>
 
 #include "pulsegrid/pipeline.hpp"
@@ -36,6 +40,17 @@ int main(int argc, char** argv) {
         const bool rfi = argc == 11 && std::atoi(argv[10]) != 0;  // reference defaults when on
         p.rfi_narrowband = rfi;
         p.rfi_broadband = rfi;
+        std::FILE* tf = nullptr;
+        std::mutex tf_mu;
+        if (const char* tp = std::getenv("PG_TIMING_OUT")) {
+            tf = std::fopen(tp, "w");
+            if (!tf) throw std::runtime_error("cannot open PG_TIMING_OUT");
+            p.engine.timing_sink = [&](const TrialTiming& t) {
+                std::lock_guard<std::mutex> lk(tf_mu);
+                std::fprintf(tf, "%zu %.6f %.6f %.6f %.6f %.6f\n", t.trial, t.dedisperse_ms, t.baseline_ms,
+                             t.normalize_ms, t.boxcar_ms, t.peaks_ms);
+            };
+        }
         auto task = create_task(argv[1], p, argv[2]);
         BufferPool pool(p.engine.memory_budget);
         auto out = execute_task(task, pool);
@@ -43,6 +58,7 @@ int main(int argc, char** argv) {
                     "\"dm_loop_ms\": %.3f, \"cluster_ms\": %.3f, \"skipped\": %zu}\n",
                     out.candidates, task.chunks.size(), out.wall_ms, out.read_ms, out.dm_loop_ms,
                     out.cluster_ms, out.skipped_trials.size());
+        if (tf) std::fclose(tf);
         return 0;
     } catch (const std::exception& e) {
         std::fprintf(stderr, "error: %s\n", e.what());

@@ -60,6 +60,7 @@ SIGNATURES = {
     "pgb_last_dedisp_time": ([_vp, _P(_c.c_double), _P(_u64), _P(_u64)], _int),
     "pgb_stream": ([_vp, _P(_vp)], _int),
     "pgb_last_cluster_ms": ([_vp, _P(_c.c_double)], _int),
+    "pgb_last_stage_times": ([_vp, _P(_c.c_double)], _int),
     "pgb_microbench_add_peak": ([_int, _P(_c.c_double), _vp], _int),
     "pgb_stream_begin": ([_vp, _u64, _vp, _sz, _P(abi.EngineConfigC), _P(abi.LinkRadiiC),
                           _P(abi.RfiConfigC)], _int),

@@ -111,6 +111,9 @@ struct pgb_context {
     cudaStream_t copy_st = nullptr;
     cudaStream_t rms_st = nullptr;  // robust RMS of chunk k overlaps the boxcar of chunk k-1
     cudaEvent_t ev_dd0[2] = {}, ev_dd1[2] = {}, ev_front[2] = {}, ev_rms[2] = {};
+    // per-stage timing of the synchronous run_dm_loop path (TrialTiming, engine.hpp:16-23):
+    // RMS start on rms_st, boxcar start / end and the end of the run order on the main stream
+    cudaEvent_t ev_rms0[2] = {}, ev_bx0 = nullptr, ev_bx1 = nullptr, ev_pk1 = nullptr;
     std::vector<cudaEvent_t> seg_events;
     std::vector<cudaEvent_t> sub_events;                 // first chunk's upload pieces
     std::vector<std::pair<uint64_t, cudaEvent_t>> prog;  // (end sample, event) of those pieces
@@ -183,6 +186,8 @@ struct pgb_context {
     uint64_t dedisp_launches = 0;
     uint64_t channel_adds = 0;
     double cluster_ms = 0.0;  // file-level sort + link_grid of the last file search (host clock)
+    // last run_dm_loop: device ms of {dedisperse, baseline, normalize, boxcar, peaks}
+    double stage_ms[5] = {};
     // last chunk's row geometry for stage fetches
     uint64_t last_out_pitch = 0;
     uint32_t last_nrows = 0;
@@ -707,6 +712,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     cudaStream_t rst = rms_main ? st : ctx->rms_st;
     PGB_CUDA(cudaEventRecord(ctx->ev_front[slot], st));
     PGB_CUDA(cudaStreamWaitEvent(rst, ctx->ev_front[slot], 0));
+    PGB_CUDA(cudaEventRecord(ctx->ev_rms0[slot], rst));
     launch_rms(work, kind, d_len, nrows, out_pitch, ctx->frms[slot].as<float>(),
                ctx->status[slot].as<uint8_t>(), in.more && !rms_main, rst);
     PGB_CUDA(cudaEventRecord(ctx->ev_rms[slot], rst));
@@ -747,6 +753,7 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
     const void* work = run.work;
     const std::vector<uint32_t>& active = run.active;
     PGB_CUDA(cudaStreamWaitEvent(st, ctx->ev_rms[slot], 0));
+    PGB_CUDA(cudaEventRecord(ctx->ev_bx0, st));
 
     // 5. boxcar ladder + runs (re-run with larger buffers on overflow)
     ChainParams cp{};
@@ -766,12 +773,14 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
         ctx->cands_raw.reserve(ctx->cand_cap * sizeof(pgb_candidate));
         ctx->frags.reserve(ctx->frag_cap * sizeof(Fragment));
         PGB_CUDA(cudaMemsetAsync(dcnt, 0, 2 * sizeof(unsigned long long), st));
+        if (attempt) PGB_CUDA(cudaEventRecord(ctx->ev_bx0, st));  // time the final attempt
         launch_boxcar_peaks(work, kind, ctx->d_row_len[slot].as<uint32_t>(), ctx->frms[slot].as<float>(),
                             ctx->status[slot].as<uint8_t>(), nrows, out_pitch, max_n, cp,
                             ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
                             ctx->d_scale.as<double>(), ctx->cands_raw.as<pgb_candidate>(), dcnt,
                             ctx->cand_cap, ctx->frags.as<Fragment>(), dcnt + 1, ctx->frag_cap,
                             box_levels(ctx, cfg->boxcar_max, nrows, out_pitch), st);
+        PGB_CUDA(cudaEventRecord(ctx->ev_bx1, st));
         PGB_CUDA(cudaMemcpyAsync(hcnt, dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         PGB_CUDA(cudaStreamSynchronize(st));
         const uint64_t nc = hcnt[0], nf = hcnt[1];
@@ -819,6 +828,7 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
                         ctx->sort_idx.as<uint32_t>() + nc, st);
         ctx->launches += 3;
     }
+    PGB_CUDA(cudaEventRecord(ctx->ev_pk1, st));
     // 7. degenerate trials (src/engine.cpp:189-194) join the uncoverable ones
     std::vector<uint8_t> stat(nrows);
     PGB_CUDA(cudaMemcpyAsync(stat.data(), ctx->status[slot].p, nrows, cudaMemcpyDeviceToHost, st));
@@ -829,6 +839,15 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
     float ms = 0.f;
     PGB_CUDA(cudaEventElapsedTime(&ms, ctx->ev_dd0[slot], ctx->ev_dd1[slot]));
     ctx->dedisp_ms += ms;
+    {  // stage times of this chunk (device clock): dedispersion, baseline, RMS, ladder, runs
+        float t[4] = {};
+        PGB_CUDA(cudaEventElapsedTime(&t[0], ctx->ev_dd1[slot], ctx->ev_front[slot]));
+        PGB_CUDA(cudaEventElapsedTime(&t[1], ctx->ev_rms0[slot], ctx->ev_rms[slot]));
+        PGB_CUDA(cudaEventElapsedTime(&t[2], ctx->ev_bx0, ctx->ev_bx1));
+        PGB_CUDA(cudaEventElapsedTime(&t[3], ctx->ev_bx1, ctx->ev_pk1));
+        ctx->stage_ms[0] = ms;
+        for (int k = 0; k < 4; ++k) ctx->stage_ms[k + 1] = t[k];
+    }
     ctx->last_out_pitch = out_pitch;
     ctx->last_nrows = nrows;
     ctx->last_had_baseline = run.baseline;
@@ -985,32 +1004,6 @@ ChunkInput prepare_f32(pgb_context* ctx, const float* dptr, uint64_t length) {
 
 // Parallel host repack of a float chunk into bytes; false if any cell is not an integer
 // in [0, 255] (then the caller uploads the floats and takes the fp32 path).
-bool host_pack_u8(const float* src, size_t n, uint8_t* dst) {
-    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const size_t nt = std::min<size_t>(std::min<unsigned>(hw, 16u), std::max<size_t>(1, n >> 22));
-    std::atomic<bool> ok{true};
-    auto work = [&](size_t a, size_t b) {
-        constexpr size_t kBlk = 1 << 14;
-        for (size_t i = a; i < b && ok.load(std::memory_order_relaxed); i += kBlk) {
-            const size_t e = std::min(b, i + kBlk);
-            bool good = true;
-            for (size_t j = i; j < e; ++j) {
-                const float v = src[j];
-                const uint8_t q = (uint8_t)(int)v;
-                good &= (v >= 0.f) & (v <= 255.f) & ((float)q == v);
-                dst[j] = q;
-            }
-            if (!good) ok.store(false, std::memory_order_relaxed);
-        }
-    };
-    std::vector<std::thread> th;
-    const size_t per = (n + nt - 1) / nt;
-    for (size_t t = 1; t < nt; ++t) th.emplace_back(work, std::min(n, t * per), std::min(n, (t + 1) * per));
-    work(0, std::min(n, per));
-    for (auto& x : th) x.join();
-    return ok.load();
-}
-
 RfiParams to_rfi(const pgb_rfi_config* r) {
     return RfiParams{r->narrowband, r->broadband, r->local_mean, r->k_sigma, r->k_mad};
 }
@@ -1023,6 +1016,7 @@ void reset_timing(pgb_context* ctx) {
     ctx->dedisp_ms = 0.0;
     ctx->dedisp_launches = 0;
     ctx->channel_adds = 0;
+    for (double& v : ctx->stage_ms) v = 0.0;
 }
 
 }  // namespace
@@ -1121,9 +1115,13 @@ pgb_status pgb_create(int device, pgb_context** out) {
         for (int k = 0; k < 2; ++k) {
             PGB_CUDA(cudaEventCreate(&ctx->ev_dd0[k]));
             PGB_CUDA(cudaEventCreate(&ctx->ev_dd1[k]));
-            PGB_CUDA(cudaEventCreateWithFlags(&ctx->ev_front[k], cudaEventDisableTiming));
-            PGB_CUDA(cudaEventCreateWithFlags(&ctx->ev_rms[k], cudaEventDisableTiming));
+            PGB_CUDA(cudaEventCreate(&ctx->ev_front[k]));
+            PGB_CUDA(cudaEventCreate(&ctx->ev_rms[k]));
+            PGB_CUDA(cudaEventCreate(&ctx->ev_rms0[k]));
         }
+        PGB_CUDA(cudaEventCreate(&ctx->ev_bx0));
+        PGB_CUDA(cudaEventCreate(&ctx->ev_bx1));
+        PGB_CUDA(cudaEventCreate(&ctx->ev_pk1));
         *out = ctx;
     });
 }
@@ -1167,8 +1165,9 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         }
         delete ctx->stream.runs;
         for (int k = 0; k < 2; ++k)
-            for (cudaEvent_t e : {ctx->ev_dd0[k], ctx->ev_dd1[k], ctx->ev_front[k], ctx->ev_rms[k]})
+            for (cudaEvent_t e : {ctx->ev_dd0[k], ctx->ev_dd1[k], ctx->ev_front[k], ctx->ev_rms[k], ctx->ev_rms0[k]})
                 cudaEventDestroy(e);
+        for (cudaEvent_t e : {ctx->ev_bx0, ctx->ev_bx1, ctx->ev_pk1}) cudaEventDestroy(e);
         cudaStreamDestroy(ctx->rms_st);
         cudaStreamDestroy(ctx->st);
         cudaStreamDestroy(ctx->copy_st);
@@ -1681,6 +1680,13 @@ pgb_status pgb_last_dedisp_time(pgb_context* ctx, double* ms, uint64_t* launches
         if (ms) *ms = ctx->dedisp_ms;
         if (launches) *launches = ctx->dedisp_launches;
         if (adds) *adds = ctx->channel_adds;
+    });
+}
+
+pgb_status pgb_last_stage_times(pgb_context* ctx, double* ms) {
+    return guarded([&] {
+        need(ctx && ms, PGB_ERR_ARGUMENT, "null argument");
+        for (int k = 0; k < 5; ++k) ms[k] = ctx->stage_ms[k];
     });
 }
 

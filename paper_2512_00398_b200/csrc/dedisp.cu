@@ -307,6 +307,27 @@ __device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
 
 constexpr int RING_NS = 3;
 
+#ifdef PGB_ABLATIONS
+// Warp-drift stress (PGB_RING_JITTER=seed, ablation library only): a pseudo-random eighth of
+// the (CTA, warp, stage, site) points sleep up to ~2 us, so warps reach the ring's full /
+// empty handshakes in scrambled orders and up to the ring's depth apart.  The tests run it
+// against the product path bit for bit (racecheck cannot model mbarrier ordering).
+__device__ __forceinline__ void ring_jitter(uint32_t seed, uint32_t gi, uint32_t site) {
+    if (!seed) return;
+    uint32_t h = seed ^ (blockIdx.x * 0x9E3779B9u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu) ^
+                 (gi * 0xC2B2AE35u) ^ (site * 0x27D4EB2Fu);
+    h ^= h >> 15;
+    h *= 0x2C1B3C6Du;
+    h ^= h >> 12;
+    h *= 0x297A2D39u;
+    h ^= h >> 15;
+    if ((h & 7) == 0) __nanosleep((h >> 16) & 2047);
+}
+#define PGB_RING_JITTER(gi, site) ring_jitter(p.jitter, (gi), (site))
+#else
+#define PGB_RING_JITTER(gi, site) ((void)0)
+#endif
+
 // MODE bits: 8 (default, G >= 2) = channel pairs, every word accumulated as K += PRMT(w0) +
 // PRMT(w1) (one IADD3) and T += w0, w1 (two IMADs): 2.5 instructions per word-add, ALU 1.5 /
 // FMA 1 (16 with 8: T by IADD3 on even words, ALU-heavier; ablation).  4 = odd words accumulate K += (w >> 8) & 0x00ff00ff (one PRMT) and
@@ -471,11 +492,15 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
     }
     uint2 wnext = nstages > D ? __ldg(wintab + (size_t)D * G + my_cs) : make_uint2(0, 0);
     const uint32_t stages_per_flush = DD_FLUSH_CH / G;
-    uint32_t since_flush = 0;
     int slot = 0, slot2 = (int)D;     // gi % NS, (gi + D) % NS
     uint32_t ph = 0, ph_prev = 0;     // parity of stage gi's use of its slot; of stage gi-1's
 
-    for (uint32_t gi = 0; gi < nstages; ++gi) {
+    // flush periods outside, their stages inside: the accumulators stay in place across the
+    // inner loop's back edge (a flush test inside one flat loop cost 16 register moves per stage)
+    for (uint32_t g0 = 0; g0 < nstages; g0 += stages_per_flush) {
+    const uint32_t g1 = min(g0 + stages_per_flush, nstages);
+    for (uint32_t gi = g0; gi < g1; ++gi) {
+        PGB_RING_JITTER(gi, 0);
         const bool pre = gi + D < nstages;
         const uint2 wstage = wnext;
         if (pre) {
@@ -540,19 +565,18 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
         }
         __syncwarp();
         if (lane == 0) ring_arrive(empty + slot);
+        PGB_RING_JITTER(gi, 1);
         if (pre) {
             // slot2 last held stage gi-1: every warp must be done adding it
             if (gi >= 1) ring_wait(empty + slot2, ph_prev);
             store_stage(slot2, wstage);
         }
-        if (++since_flush == stages_per_flush || gi + 1 == nstages) {
-            flush();
-            since_flush = 0;
-        }
         // advance ring indices: stage gi+1 uses slot (gi+1)%NS, use count (gi+1)/NS
         ph_prev = ph;
         if (++slot == NS) { slot = 0; ph ^= 1; }
         if (++slot2 == NS) slot2 = 0;
+    }
+    flush();
     }
     // the barriers are re-initialised for the next (block, tile) item: invalidate them
     // once every warp is past its last wait on them
@@ -1239,7 +1263,12 @@ size_t ring_smem_bytes(int g, uint32_t wmax, int ns = RING_NS) {
 }
 
 #ifdef PGB_ABLATIONS
-void launch_dedisp_u8_ablation(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st) {
+void launch_dedisp_u8_ablation(const DedispLaunch& p0, const uint8_t* rows, int32_t* out, cudaStream_t st) {
+    DedispLaunch p = p0;
+    {
+        const char* j = pgb_ablation_env("PGB_RING_JITTER");
+        p.jitter = j ? (uint32_t)strtoul(j, nullptr, 10) : 0u;
+    }
     const size_t smem = dedisp_smem_bytes(true, p.g, p.wmax);
     const int tb = DD_WARPS * p.tpw;
     dim3 grid((p.nrows + tb - 1) / tb, p.ntiles - p.tile0);

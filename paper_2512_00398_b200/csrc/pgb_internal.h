@@ -71,6 +71,10 @@ struct PinnedBuf {
 // ---- kernel tiling constants ----------------------------------------------------
 
 // Dedispersion CTA tile: DD_TB trials x DD_NT output samples, 16 warps.
+// host_pack.cpp: widened 8-bit float cells -> bytes (false if any cell is not an integer
+// in [0, 255]; the caller then keeps the fp32 path)
+bool host_pack_u8(const float* src, size_t n, uint8_t* dst);
+
 constexpr int DD_THREADS = 512;
 constexpr int DD_WARPS = DD_THREADS / 32;
 constexpr int DD_NT = 1024;             // outputs per tile
@@ -153,6 +157,7 @@ struct DedispLaunch {
     const uint32_t* blk_first;  // [nblocks] or null
     uint32_t tile0;
     uint32_t* work_ctr;         // persistent ring kernel: zeroed item counter (or null)
+    uint32_t jitter;            // ablation builds only: seed of the ring's warp-drift stress (0 = off)
 };
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st);
 // builds p.dd_win / p.dd_off for the active set (tile independent; p.wmax = bytes per copy)

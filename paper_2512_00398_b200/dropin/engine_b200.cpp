@@ -143,7 +143,8 @@ DmLoopResult run_dm_loop(const Chunk& chunk, const DmTrialPlan& plan, const Engi
                                cfg.boxcar_max,    cfg.baseline_window,      cfg.memory_budget,
                                cfg.max_in_flight};
     std::size_t nc = 0, ns = 0;
-    // widened chunk (floats); integral 8-bit data is detected and repacked on the device
+    // widened chunk (floats): integral 8-bit data is repacked to bytes on the host and
+    // uploaded from pinned memory (a quarter of the bytes); anything else stays fp32
     check(pgb_run_dm_loop_f32(tc.ctx, chunk.data.data(), 0, &spec, &ec, &nc, &ns));
     DmLoopResult result;
     result.candidates.resize(nc);
@@ -151,14 +152,31 @@ DmLoopResult run_dm_loop(const Chunk& chunk, const DmTrialPlan& plan, const Engi
     std::vector<std::uint64_t> sk(ns);
     check(pgb_fetch_skipped(tc.ctx, sk.data(), ns));
     result.skipped_trials.assign(sk.begin(), sk.end());
-    if (cfg.timing_sink) {  // device stages amortized per trial (engine.hpp:14-23)
-        double ms = 0.0;
-        std::uint64_t launches = 0, adds = 0;
-        check(pgb_last_dedisp_time(tc.ctx, &ms, &launches, &adds));
+    if (cfg.timing_sink) {
+        // The device runs each stage batched over the chunk's trials; like the reference's
+        // per-block dedisperse_ms (src/engine.cpp:147-149), every stage time is amortised
+        // over the trials it processed, and only trials that reached the end of the chain
+        // emit a record (uncoverable and degenerate ones do not, src/engine.cpp:112-118,
+        // 189-194)
+        double ms[5] = {};
+        check(pgb_last_stage_times(tc.ctx, ms));
+        std::vector<std::size_t> done;
+        done.reserve(plan.ntrials());
+        std::size_t k = 0;
         for (std::size_t t = 0; t < plan.ntrials(); ++t) {
+            while (k < result.skipped_trials.size() && result.skipped_trials[k] < t) ++k;
+            if (k < result.skipped_trials.size() && result.skipped_trials[k] == t) continue;
+            done.push_back(t);
+        }
+        const double inv = done.empty() ? 0.0 : 1.0 / double(done.size());
+        for (std::size_t t : done) {
             TrialTiming timing;
             timing.trial = t;
-            timing.dedisperse_ms = ms / double(plan.ntrials());
+            timing.dedisperse_ms = ms[0] * inv;
+            timing.baseline_ms = cfg.baseline_window > 0 ? ms[1] * inv : 0.0;
+            timing.normalize_ms = ms[2] * inv;
+            timing.boxcar_ms = ms[3] * inv;
+            timing.peaks_ms = ms[4] * inv;
             cfg.timing_sink(timing);
         }
     }

@@ -301,11 +301,18 @@ class Engine:
         skipped = np.zeros(ns.value, np.uint64)
         self._check(self._lib.pgb_fetch_skipped(self._h, abi.ptr(skipped), ns.value))
         if cfg.timing_sink is not None:
-            ms, _, _ = self.last_dedisp_time()
+            # stage times batched over the chunk, amortised over the trials that finished
+            # the chain; skipped trials emit nothing (src/engine.cpp:112-118, 147-213)
+            ms = (ctypes.c_double * 5)()
+            self._check(self._lib.pgb_last_stage_times(self._h, ms))
             lo, hi = self._range
-            per = ms / max(1, hi - lo)
-            for t in range(lo, hi):
-                cfg.timing_sink(TrialTiming(trial=t, dedisperse_ms=per))
+            done = np.setdiff1d(np.arange(lo, hi, dtype=np.uint64), skipped)
+            inv = 1.0 / max(1, len(done))
+            for t in done:
+                cfg.timing_sink(TrialTiming(trial=int(t), dedisperse_ms=ms[0] * inv,
+                                            baseline_ms=ms[1] * inv if cfg.baseline_window > 0 else 0.0,
+                                            normalize_ms=ms[2] * inv, boxcar_ms=ms[3] * inv,
+                                            peaks_ms=ms[4] * inv))
         return DmLoopResult(cands, skipped)
 
     # ---- dedispersion only --------------------------------------------------------

@@ -67,6 +67,29 @@ def test_link_substitution_u8(ref, tmp_path):
     assert write_candidates(res.clusters) == ref_text
 
 
+def test_timing_sink_records_processed_trials(ref, tmp_path, monkeypatch):
+    """EngineConfig::timing_sink (engine.hpp:16-23): the drop-in emits one TrialTiming per
+    trial that finished the chain in each chunk -- the same multiset of trial ids as the
+    reference's execute_task -- with the device stage times amortised over them."""
+    _need_binaries()
+    fil = tmp_path / "u8.fil"
+    _u8_file(ref, fil)
+    recs = {}
+    for binary in ("pipeline_ref", "pipeline_b200"):
+        out = tmp_path / f"{binary}.timing"
+        monkeypatch.setenv("PG_TIMING_OUT", str(out))
+        _run(binary, fil, tmp_path / f"{binary}.cand", ARGS_U8)
+        rows = [line.split() for line in out.read_text().splitlines()]
+        recs[binary] = ([int(r[0]) for r in rows], [[float(v) for v in r[1:]] for r in rows])
+    ref_trials, _ = recs["pipeline_ref"]
+    b_trials, b_ms = recs["pipeline_b200"]
+    assert len(ref_trials) > 0
+    assert sorted(b_trials) == sorted(ref_trials)
+    ms = np.asarray(b_ms)
+    assert (ms >= 0).all() and (ms[:, 0] > 0).all() and (ms[:, 2] > 0).all() and (ms[:, 3] > 0).all()
+    assert (ms[:, 1] > 0).all()  # baseline on (baseline_s = 0.5)
+
+
 def test_link_substitution_f32_file(ref, tmp_path):
     """nbits=32 Gaussian file (tests/test_pipeline.cpp:24-35 style): the fp32 in-order path."""
     _need_binaries()

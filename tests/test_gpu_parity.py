@@ -269,6 +269,26 @@ def test_uncoverable_trials_are_skipped(engine, ref):
     assert [t not in set(res.skipped_trials.tolist()) for t in range(plan.ntrials)] == fits
 
 
+def test_timing_sink_skips_unprocessed_trials(engine, ref):
+    """EngineConfig.timing_sink: one TrialTiming per trial that finished the chain, with the
+    batched device stage times amortised over them (src/engine.cpp:147-213)."""
+    from dataclasses import replace
+
+    hdr = FilterbankHeader(fch1=1500.0, foff=-2.0, nchans=32, tsamp=64e-6)
+    g = ref.generate_noise(1500.0, -2.0, 64e-6, 32, 1024, 0.0, 1.0, 78)
+    plan = generate_dm_trials(0.0, 2000.0, hdr, LinearSpacing(500.0))
+    recs = []
+    cfg = replace(EngineConfig(n_workers=2, tsamp=hdr.tsamp, boxcar_max=64, baseline_window=101),
+                  timing_sink=recs.append)
+    res = engine.run_dm_loop(Chunk(ChunkSpec.whole(1024), g), plan, cfg)
+    done = [t for t in range(plan.ntrials) if t not in set(res.skipped_trials.tolist())]
+    assert 0 < len(done) < plan.ntrials
+    assert [r.trial for r in recs] == done
+    for r in recs:
+        assert r.dedisperse_ms > 0 and r.baseline_ms > 0 and r.normalize_ms > 0 and r.boxcar_ms > 0
+        assert r.peaks_ms >= 0
+
+
 def test_config_errors(engine):
     hdr, plan, data = _small_u8_case()
     spec = ChunkSpec.whole(data.shape[0])

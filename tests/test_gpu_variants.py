@@ -49,6 +49,11 @@ print("ok")
     {"PGB_RING_MODE": "4"},               # odd words as (PRMT, IMAD, IMAD), even words as mode 0
     {"PGB_RING_MODE": "24"},              # channel pairs, T by IADD3 on even words
     {"PGB_F32_RING0": "1"},               # fp32 two-barrier kernel
+    # mbarrier-ring race stress: random per-warp sleeps around the full / empty handshakes
+    # scramble the warps' arrival order (racecheck does not model mbarrier acquire/release)
+    {"PGB_RING_JITTER": "1"},
+    {"PGB_RING_JITTER": "987654321"},
+    {"PGB_RING_JITTER": "5", "PGB_DD_PERSIST0": "1"},
 ])
 def test_dedispersion_variants_bit_exact(env):
     e = dict(os.environ, **env)

@@ -70,3 +70,21 @@ def test_baseline_window_rounding():
     assert baseline_window_samples(2.0, 49.152e-6) == 40691
     assert baseline_window_samples(0.0, 64e-6) == 0
     assert baseline_window_samples(1e-9, 64e-6) == 1
+
+
+def test_host_pack_u8_round_trip(tmp_path):
+    """The drop-in's host repack of widened 8-bit chunks (csrc/host_pack.cpp, AVX2 + scalar):
+    exact bytes for integral cells, failure for any other cell (tests/cpp/host_pack_check.cpp)."""
+    import shutil
+    import subprocess
+    from pathlib import Path
+
+    root = Path(__file__).resolve().parents[1]
+    src = root / "paper_2512_00398_b200" / "csrc" / "host_pack.cpp"
+    if not shutil.which("g++"):
+        pytest.skip("no g++")
+    exe = tmp_path / "pack_check"
+    subprocess.run(["g++", "-O2", "-std=c++17", "-pthread", str(root / "tests" / "cpp" / "host_pack_check.cpp"),
+                    str(src), "-o", str(exe)], check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0 and "pack ok" in out.stdout, out.stdout + out.stderr

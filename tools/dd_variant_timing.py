@@ -1,5 +1,5 @@
 """Dedispersion kernel time for one config-B chunk under the current environment
-(variant switches such as PGB_DD_HHI / PGB_DD_SFMA): CUDA-event time of the dedispersion
+(variant switches such as PGB_RING_MODE select the ablation library): CUDA-event time of the dedispersion
 launch, best of N runs after a warm-up.  Usage: python tools/dd_variant_timing.py [reps]"""
 import os
 import sys
@@ -19,7 +19,7 @@ payload = bench.make_payload(cfg, task.plan, rows=spec.length)
 torch.cuda.synchronize()
 reps = int(sys.argv[1]) if len(sys.argv) > 1 else 5
 env = {k: v for k, v in os.environ.items() if k.startswith("PGB_")}
-with Engine(0) as eng:
+with Engine(0, ablations=bool(env)) as eng:
     ts = []
     for _ in range(reps + 1):
         res = eng.run_dm_loop(Chunk(spec, payload), task.plan, task.engine)
