@@ -338,12 +338,13 @@ __device__ __forceinline__ void ring_jitter(uint32_t seed, uint32_t gi, uint32_t
 // the FMA pipe (mul.hi + mad.lo funnel) instead of PRMT on the ALU pipe; 2 = per-(channel,
 // trial) shared-memory addresses formed with IMAD (FMA pipe) instead of IADD (ALU pipe)
 // One (trial block, time tile) of the ring kernel; the whole CTA calls it.
-template <int G, int VPT, int MODE, int NS = RING_NS>
+// NW = warps per CTA (16: two trials per warp; 32: one trial per warp, ablation).
+template <int G, int VPT, int MODE, int NS = RING_NS, int NW = DD_WARPS>
 __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* __restrict__ rows,
                                           int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len,
                                           const uint32_t blk, const uint32_t tile) {
-    constexpr int TPW = 2;
-    constexpr int TB = DD_WARPS * TPW;
+    constexpr int TPW = 32 / NW;
+    constexpr int TB = NW * TPW;
     static_assert(TB == 32, "table layout assumes 32-trial blocks");
     static_assert(NS == 2 || NS == 3, "ring depth");
     constexpr uint32_t D = NS - 1;  // stages loaded ahead
@@ -360,7 +361,7 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const uint32_t nstages = p.nchans_pad / G;
-    constexpr int wpc = DD_WARPS / G;
+    constexpr int wpc = NW / G;
     const int my_cs = warp / wpc;
     const uint32_t my_t = (uint32_t)((warp % wpc) * 32 + lane);
     constexpr uint32_t vstride = (uint32_t)wpc * 32;
@@ -373,8 +374,8 @@ __device__ __forceinline__ void ring_tile(const DedispLaunch& p, const uint8_t* 
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < NS; ++s) {
-            ring_init(full + s, DD_WARPS);
-            ring_init(empty + s, DD_WARPS);
+            ring_init(full + s, NW);
+            ring_init(empty + s, NW);
         }
     }
     __syncthreads();
@@ -605,8 +606,8 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 // Persistent variant: one CTA per SM takes (block, tile) items from a counter in the
 // grid's order (blocks fastest), so the last wave is not quantised to whole CTAs of a
 // 7-55-wave grid (the tail is ~1 % of a launch with 8192 CTAs, several % with 1024).
-template <int G, int VPT, int NS = RING_NS, int MODE = 0>
-__global__ void __launch_bounds__(DD_THREADS, 1)
+template <int G, int VPT, int NS = RING_NS, int MODE = 0, int NW = DD_WARPS>
+__global__ void __launch_bounds__(NW * 32, 1)
     dedisp_u8_ring_persist_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
                                   int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
     __shared__ uint32_t s_item;
@@ -621,7 +622,7 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
         const uint32_t blk = item % nblocks, tile = p.tile0 + item / nblocks;
         if (p.blk_first && tile < p.blk_first[blk]) continue;
         if ((uint64_t)tile * DD_NT >= blk_len[blk]) continue;
-        ring_tile<G, VPT, MODE, NS>(p, rows, out, blk_len, blk, tile);
+        ring_tile<G, VPT, MODE, NS, NW>(p, rows, out, blk_len, blk, tile);
     }
 }
 
@@ -1298,6 +1299,31 @@ void launch_dedisp_u8_ablation(const DedispLaunch& p0, const uint8_t* rows, int3
         const char* e = pgb_ablation_env("PGB_RING_MODE");
         return e ? atoi(e) & 31 : 8;  // default: channel-paired (K, T) accumulation (8)
     }();
+    static const int nw32 = [] {  // PGB_DD_WARPS=32: 1024-thread ring, one trial per warp
+        const char* e = pgb_ablation_env("PGB_DD_WARPS");
+        return e && atoi(e) == 32;
+    }();
+    if (ring && !v1 && !sf && p.tpw == 2 && p.dd_off && nw32 && p.work_ctr) {
+        int g = 8;
+        while (g > 1 && ring_smem_bytes(g, p.wmax) > 227 * 1024) g >>= 1;
+        const size_t rsm = ring_smem_bytes(g, p.wmax);
+        const int vpt = (int)((p.wmax / 16 + 32u * (32 / g) - 1) / (32u * (32 / g)));
+        if (rsm <= 227 * 1024 && g >= p.g) {
+#define PGB_RING32(G_, V_)                                                                           \
+    if (g == G_ && vpt <= V_) {                                                                      \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist_kernel<G_, V_, RING_NS, 8, 32>,         \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));       \
+        dedisp_u8_ring_persist_kernel<G_, V_, RING_NS, 8, 32><<<num_sms(), 1024, rsm, st>>>(         \
+            p, rows, out, p.blk_len);                                                                \
+        dd_which("ring3-persist-1024", G_, V_, 8);                                                   \
+        PGB_CUDA(cudaGetLastError());                                                                \
+        return;                                                                                      \
+    }
+            PGB_RING32(8, 1) PGB_RING32(8, 2) PGB_RING32(8, 4)
+            PGB_RING32(4, 1) PGB_RING32(4, 2) PGB_RING32(4, 4)
+#undef PGB_RING32
+        }
+    }
     if (ring && !v1 && !sf && p.tpw == 2 && p.dd_off) {
         int g = 8;
         while (g > 1 && ring_smem_bytes(g, p.wmax) > 227 * 1024) g >>= 1;

@@ -54,6 +54,8 @@ print("ok")
     {"PGB_RING_JITTER": "1"},
     {"PGB_RING_JITTER": "987654321"},
     {"PGB_RING_JITTER": "5", "PGB_DD_PERSIST0": "1"},
+    {"PGB_DD_WARPS": "32"},               # 1024-thread ring, one trial per warp
+    {"PGB_DD_WARPS": "32", "PGB_RING_JITTER": "3"},
 ])
 def test_dedispersion_variants_bit_exact(env):
     e = dict(os.environ, **env)
