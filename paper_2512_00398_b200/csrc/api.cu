@@ -18,6 +18,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <functional>
 
 #include "pgb_internal.h"
 
@@ -143,8 +144,11 @@ struct pgb_context {
     bool ser_ok = false;
     uint64_t ser_start = 0, ser_len = 0, ser_pitch = 0;
     uint32_t dd_tab_wmax = 0;  // wmax the staging table was built for (0 = stale)
-    DevBuf ddf_win, ddf_off;     // f32 staging table (RFI-masked, non-integer chunks)
+    DevBuf ddf_win, ddf_off;     // f32 staging table (non-integer float chunks)
     uint32_t ddf_tab_wmax = 0;
+    DevBuf ddh_win, ddh_off;     // fp16 staging table (RFI-masked 8-bit chunks with float rows)
+    uint32_t ddh_tab_wmax = 0;
+    std::vector<uint32_t> bad_rows_host;  // the current chunk's flagged rows (exception density)
     DevBuf file_cands, file_sorted;
     // asynchronous file-search back halves: {candidate total, high-water nc, nf}, the
     // per-chunk degenerate-trial flags (pinned) and per-chunk dedispersion events
@@ -251,6 +255,15 @@ struct ChunkInput {
     const std::vector<std::pair<uint64_t, cudaEvent_t>>* prog = nullptr;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;  // dedispersion timing events (else the slot's)
     uint64_t pitch_min = 0;   // series pitch floor (a file search keeps one pitch for all chunks)
+    // RFI-masked 8-bit chunk (data = the raw codes, src/rfi.cpp:93-139): the transpose zeroes
+    // the bad channels and bad rows; with local-mean replacement (h16) the bad rows' float
+    // values come from ctx->rfi's exception lists and the fp16 in-order kernel runs, unless
+    // the geometry or the flag density does not fit it -- then fallback() widens the masked
+    // chunk to floats (the fp32 path)
+    const uint8_t* chan_bad = nullptr;
+    const uint8_t* samp_bad = nullptr;
+    bool h16 = false;
+    std::function<ChunkInput()> fallback;
 };
 
 // Validation and in-flight arithmetic of run_dm_loop (src/engine.cpp:60-97).
@@ -425,12 +438,14 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         ctx->geom_valid = true;
         ctx->dd_tab_wmax = 0;
         ctx->ddf_tab_wmax = 0;
+        ctx->ddh_tab_wmax = 0;
         ctx->d_active.reserve(nrows * sizeof(uint32_t));
         stage_h2d(ctx, ctx->d_active.p, active.data(), nrows * sizeof(uint32_t), st);
     }
     std::vector<uint32_t> blk_len(nblocks, 0);
     for (uint32_t r = 0; r < nrows; ++r) blk_len[r / tb] = std::max(blk_len[r / tb], row_len[r]);
     const bool u8 = in.u8;
+    const bool h16 = in.h16;  // RFI-masked 8-bit chunk with float rows: the fp16 in-order kernel
     if (u8 && C > PGB_MAX_EXACT_CHANS)
         raise(PGB_ERR_CONFIG, "8-bit input with more than 65793 channels: the integer channel sums pass "
                               "2^24, where the reference's fp32 sums start rounding (widen to floats)");
@@ -440,7 +455,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     uint32_t spread = 0;
     std::vector<uint32_t> wide_rows;
     for (uint32_t b = 0; b < nblocks; ++b) {
-        if (dedisp_staged_fits(u8, ctx->blk_spread[b])) {
+        if (h16 || dedisp_staged_fits(u8, ctx->blk_spread[b])) {
             spread = std::max(spread, ctx->blk_spread[b]);
         } else {
             for (uint32_t r = b * tb; r < std::min(nrows, (b + 1) * tb); ++r) wide_rows.push_back(r);
@@ -448,9 +463,35 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         }
     }
     const uint32_t align_el = u8 ? 16 : 4;
-    const uint32_t wmax = (uint32_t)round_up(spread + DD_NT + 2 * align_el + 16, 16);
+    const uint32_t wmax = h16 ? (uint32_t)round_up(spread + DD_NT + 32, 16)  // halves per copy
+                              : (uint32_t)round_up(spread + DD_NT + 2 * align_el + 16, 16);
     int g = 8;
-    while (g > 1 && dedisp_smem_bytes(u8, g, wmax) > DD_SMEM_BUDGET) g >>= 1;
+    if (h16) {
+        // every block must fit a staged window, and no window may cover more than HX_CAP
+        // flagged rows (a window of wmax + 2 rows covers R[lo..hi] iff R[hi] - R[lo] < wmax + 2)
+        g = dedisp_h16_stage_width(wmax);
+        const std::vector<uint32_t>& R = ctx->bad_rows_host;
+        size_t dense = 0;  // most flagged rows in one window
+        for (size_t lo = 0, hi = 0; hi < R.size(); ++hi) {
+            while ((uint64_t)R[hi] - R[lo] >= (uint64_t)wmax + 2) ++lo;
+            dense = std::max(dense, hi - lo + 1);
+        }
+        static const bool which = getenv("PGB_DD_WHICH") != nullptr;
+        if (which)
+            fprintf(stderr, "pgb rfi: %zu flagged rows, at most %zu per %u-row window, stage width %d\n", R.size(),
+                    dense, wmax + 2, g);
+        if (g == 0 || dense > (size_t)HX_CAP) {
+            ChunkInput fb = in.fallback();
+            fb.more = in.more;
+            fb.ev0 = in.ev0;
+            fb.ev1 = in.ev1;
+            fb.pitch_min = in.pitch_min;
+            chunk_front(ctx, fb, spec, cfg, slot, run);
+            return;
+        }
+    } else {
+        while (g > 1 && dedisp_smem_bytes(u8, g, wmax) > DD_SMEM_BUDGET) g >>= 1;
+    }
     // warp-specialized TMA kernel (u8): 16-byte aligned window starts, 256-byte boxes,
     // >= 20 bytes of slack for the packers' funnel shifts; deepest ring that fits
     int ws_g = 0, ws_ns = 0;
@@ -476,10 +517,10 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     const uint64_t out_pitch = std::max<uint64_t>((uint64_t)ntiles * DD_NT, round_up(in.pitch_min, DD_NT));
     const uint64_t rows_pitch =
         round_up((uint64_t)ntiles * DD_NT + maxd_active + std::max(wmax, ws_wmax) + 64, 64);
-    const size_t esz = u8 ? 1 : 4;
+    const size_t esz = u8 ? 1 : h16 ? 2 : 4;
 
-    const uint32_t C_pad = (C + 7) & ~7u;  // u8 rows padded with zero rows to whole 8-channel groups
-    ctx->rows.reserve((size_t)(u8 ? C_pad : C) * rows_pitch * esz, true);
+    const uint32_t C_pad = (C + 7) & ~7u;  // u8/fp16 rows padded with zero rows to whole 8-channel groups
+    ctx->rows.reserve((size_t)(u8 || h16 ? C_pad : C) * rows_pitch * esz, true);
     ctx->series.reserve((size_t)nrows * out_pitch * 4);
     const bool baseline = cfg->baseline_window > 0;
     if (baseline) ctx->base[slot].reserve((size_t)nrows * out_pitch * 4);
@@ -509,13 +550,23 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     if (in.prog && !in.prog->empty() && !progressive)  // whole chunk first
         PGB_CUDA(cudaStreamWaitEvent(st, in.prog->back().second, 0));
     if (u8) {
-        if (!progressive)
+        if (in.chan_bad)  // RFI zero mask: integer cells, bad channels and rows zeroed
+            launch_transpose_masked(static_cast<const uint8_t*>(in.data), L, C, in.chan_bad, in.samp_bad,
+                                    ctx->rows.p, rows_pitch, false, st);
+        else if (!progressive)
             launch_transpose_u8(static_cast<const uint8_t*>(in.data), L, C, ctx->rows.as<uint8_t>(),
                                 rows_pitch, st);
         trace_mark(ctx, "transpose", st);
         if (C_pad > C)
             PGB_CUDA(cudaMemsetAsync(ctx->rows.as<uint8_t>() + (size_t)C * rows_pitch, 0,
                                      (size_t)(C_pad - C) * rows_pitch, st));
+    } else if (h16) {
+        launch_transpose_masked(static_cast<const uint8_t*>(in.data), L, C, in.chan_bad, in.samp_bad,
+                                ctx->rows.p, rows_pitch, true, st);
+        trace_mark(ctx, "transpose (fp16, masked)", st);
+        if (C_pad > C)
+            PGB_CUDA(cudaMemsetAsync(ctx->rows.as<uint16_t>() + (size_t)C * rows_pitch, 0,
+                                     (size_t)(C_pad - C) * rows_pitch * 2, st));
     }
     else
         launch_transpose_f32(static_cast<const float*>(in.data), L, C, ctx->rows.as<float>(),
@@ -648,6 +699,26 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
             ctx->ser_len = L;
             ctx->ser_pitch = out_pitch;
         }
+    }
+    else if (h16) {
+        dl.nchans_pad = C_pad;
+        if (ctx->ddh_tab_wmax != wmax) {
+            ctx->ddh_win.reserve((size_t)nblocks * dl.nchans_pad * sizeof(uint2));
+            ctx->ddh_off.reserve((size_t)nblocks * dl.nchans_pad * 32 * 4);
+            launch_ddh_table(dl, ctx->ddh_win.as<uint2>(), ctx->ddh_off.as<uint32_t>(), st);
+            ctx->launches += 1;
+            ctx->ddh_tab_wmax = wmax;
+        }
+        dl.dd_win = ctx->ddh_win.as<uint2>();
+        dl.dd_off = ctx->ddh_off.as<uint32_t>();
+        dl.xP = ctx->rfi.xP.as<uint32_t>();
+        dl.xR = ctx->rfi.xR.as<uint32_t>();
+        dl.xF = ctx->rfi.xF.as<float>();
+        dl.xlen = L;
+        ctx->d_work.reserve(64 * sizeof(uint32_t), true);
+        dl.work_ctr = ctx->d_work.as<uint32_t>();
+        PGB_CUDA(cudaMemsetAsync(dl.work_ctr, 0, sizeof(uint32_t), st));
+        launch_dedisp_h16(dl, ctx->rows.as<uint16_t>(), ctx->series.as<float>(), st);
     }
     else {
         dl.nchans_pad = (C + 7) & ~7u;
@@ -1002,11 +1073,56 @@ ChunkInput prepare_f32(pgb_context* ctx, const float* dptr, uint64_t length) {
     return ChunkInput{dptr, false};
 }
 
-// Parallel host repack of a float chunk into bytes; false if any cell is not an integer
-// in [0, 255] (then the caller uploads the floats and takes the fp32 path).
 RfiParams to_rfi(const pgb_rfi_config* r) {
     return RfiParams{r->narrowband, r->broadband, r->local_mean, r->k_sigma, r->k_mad};
 }
+
+// RFI excision of an 8-bit chunk on the device (src/pipeline.cpp:79-87, src/rfi.cpp): the
+// flags, then -- if any -- the masked chunk as the dedispersion input.  Zero replacement or
+// bad channels only: integer cells, the u8 path with the transpose zeroing them.  Local-mean
+// replacement of bad rows: the fp16 in-order kernel with the rows' float values as
+// exceptions; the widened float chunk (fp32 path) only if that kernel does not fit.
+ChunkInput rfi_input(pgb_context* ctx, const uint8_t* cptr, uint64_t length, const pgb_rfi_config* rfi) {
+    const uint32_t C = ctx->nchans;
+    const RfiParams rp = to_rfi(rfi);
+    uint64_t nbc = 0, nbs = 0;
+    rfi_flags_impl<uint8_t>(cptr, length, C, rp, ctx->rfi, ctx->st, &nbc, &nbs);
+    ctx->launches += 8;
+    trace_mark(ctx, "rfi flags", ctx->st);
+    ChunkInput ci{cptr, true};
+    ci.raw = true;
+    if (!nbc && !nbs) return ci;
+    ci.raw = false;  // the mask is chunk-local: no overlap reuse
+    ci.chan_bad = ctx->rfi.chan_bad.as<uint8_t>();
+    ci.samp_bad = ctx->rfi.samp_bad.as<uint8_t>();
+    if (nbs && rp.local_mean && !pgb_ablation_env("PGB_RFI_H16")) {
+        // local-mean rows: the widened float chunk and the in-order fp32 ring (the fp16
+        // kernel with exception rows, PGB_RFI_H16=1 in the ablation library, measured
+        // slower on config E: DESIGN.md section 10)
+        ctx->rfi_out.reserve((size_t)length * C * 4);
+        rfi_mask_impl<uint8_t>(cptr, length, C, rp, ctx->rfi, ctx->rfi_out.as<float>(), ctx->st, nbc, nbs);
+        ctx->launches += 2;
+        return prepare_f32(ctx, ctx->rfi_out.as<float>(), length);
+    }
+    if (nbs && rp.local_mean) {
+        rfi_exceptions_u8(cptr, length, C, rp, ctx->rfi, nbs, ctx->st, &ctx->bad_rows_host);
+        ctx->launches += nbs ? 4 : 3;
+        trace_mark(ctx, "rfi exceptions", ctx->st);
+        ci.u8 = false;
+        ci.h16 = true;
+        ci.fallback = [ctx, cptr, length, rp, nbc, nbs]() {
+            ctx->rfi_out.reserve((size_t)length * ctx->nchans * 4);
+            rfi_mask_impl<uint8_t>(cptr, length, ctx->nchans, rp, ctx->rfi, ctx->rfi_out.as<float>(), ctx->st,
+                                   nbc, nbs);
+            ctx->launches += 2;
+            return prepare_f32(ctx, ctx->rfi_out.as<float>(), length);
+        };
+    }
+    return ci;
+}
+
+// Parallel host repack of a float chunk into bytes; false if any cell is not an integer
+// in [0, 255] (then the caller uploads the floats and takes the fp32 path).
 
 void reset_timing(pgb_context* ctx) {
     // every top-level call starts here (after the previous call's final stream sync), so
@@ -1577,17 +1693,9 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                 ci.more = overlap && k + 1 < nchunks;
                 if (prog_k) ci.prog = &ctx->prog;
                 if (rfi && (rfi->narrowband || rfi->broadband)) {  // src/pipeline.cpp:79-87
-                    uint64_t nbc = 0, nbs = 0;
-                    ctx->rfi_out.reserve((size_t)chunks[k].length * C * 4);
-                    rfi_clean_impl<uint8_t>(cptr, chunks[k].length, C, to_rfi(rfi), ctx->rfi, ctx->rfi_out.as<float>(),
-                                            ctx->st, &nbc, &nbs);
-                    ctx->launches += 8;
-                    trace_mark(ctx, "rfi excision", ctx->st);
-                    if (nbc || nbs) {
-                        ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), chunks[k].length);
-                        ci.pitch_min = pitch_min;
-                        ci.more = overlap && k + 1 < nchunks;
-                    }
+                    ci = rfi_input(ctx, cptr, chunks[k].length, rfi);
+                    ci.pitch_min = pitch_min;
+                    ci.more = overlap && k + 1 < nchunks;
                 }
                 if (async_back) {
                     ci.ev0 = ctx->file_dd_ev[2 * k];
@@ -1813,16 +1921,9 @@ pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
         ci.pitch_min = S.pitch_min;
         ci.more = S.overlap && k + 1 < S.chunks.size();
         if (S.has_rfi) {  // src/pipeline.cpp:79-87
-            uint64_t nbc = 0, nbs = 0;
-            ctx->rfi_out.reserve(cb * 4);
-            rfi_clean_impl<uint8_t>(cptr, spec.length, C, to_rfi(&S.rfi), ctx->rfi, ctx->rfi_out.as<float>(), ctx->st,
-                                    &nbc, &nbs);
-            ctx->launches += 8;
-            if (nbc || nbs) {
-                ci = prepare_f32(ctx, ctx->rfi_out.as<float>(), spec.length);
-                ci.pitch_min = S.pitch_min;
-                ci.more = S.overlap && k + 1 < S.chunks.size();
-            }
+            ci = rfi_input(ctx, cptr, spec.length, &S.rfi);
+            ci.pitch_min = S.pitch_min;
+            ci.more = S.overlap && k + 1 < S.chunks.size();
         }
         ChunkRun* runs = S.runs->r;
         ChunkRun& cur = runs[k & 1];

@@ -36,6 +36,7 @@
 
 #include <cstdio>
 
+#include "mbarrier.cuh"
 #include "pgb_internal.h"
 
 namespace pgb {
@@ -279,32 +280,6 @@ __global__ void __launch_bounds__(DD_THREADS, 1)
 // A warp only waits for the others to have finished stage g-1, so warps drift up to a
 // stage apart instead of meeting at every stage (the barrier cost ~7 ms of 51 per
 // config-B chunk: timing experiment "no barrier").
-__device__ __forceinline__ uint32_t sh_addr(const void* p) {
-    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void ring_init(uint64_t* bar, uint32_t count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sh_addr(bar)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void ring_inval(uint64_t* bar) {
-    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(sh_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void ring_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(sh_addr(bar)) : "memory");
-}
-__device__ __forceinline__ void ring_wait(uint64_t* bar, uint32_t parity) {
-    const uint32_t a = sh_addr(bar);
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%1], %2;\n\t"
-            "selp.u32 %0, 1, 0, p;\n\t}"
-            : "=r"(done)
-            : "r"(a), "r"(parity)
-            : "memory");
-    }
-}
-
 constexpr int RING_NS = 3;
 
 #ifdef PGB_ABLATIONS
@@ -1517,6 +1492,7 @@ void launch_dedisp_f32(const DedispLaunch& p, const float* rows, float* out, cud
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));    \
         dedisp_f32_ring_kernel<G_><<<grid, DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len);       \
         PGB_CUDA(cudaGetLastError());                                                             \
+        dd_which("f32-ring", G_, 0, 0);                                                           \
         return;                                                                                   \
     }
             PGB_FRING(8) PGB_FRING(4) PGB_FRING(2) PGB_FRING(1)

@@ -158,6 +158,12 @@ struct DedispLaunch {
     uint32_t tile0;
     uint32_t* work_ctr;         // persistent ring kernel: zeroed item counter (or null)
     uint32_t jitter;            // ablation builds only: seed of the ring's warp-drift stress (0 = off)
+    // fp16 kernel (RFI-masked 8-bit chunks): flagged rows staged as +0, their values added
+    // in channel order from these lists
+    const uint32_t* xP;         // [xlen + 1] bad rows before each row
+    const uint32_t* xR;         // bad rows, ascending
+    const float* xF;            // [bad row][nchans] replacement values
+    uint64_t xlen;              // chunk rows
 };
 void launch_dedisp_u8(const DedispLaunch& p, const uint8_t* rows, int32_t* out, cudaStream_t st);
 // builds p.dd_win / p.dd_off for the active set (tile independent; p.wmax = bytes per copy)
@@ -175,6 +181,16 @@ bool dedisp_staged_fits(bool u8, uint32_t spread);
 // blocks that do not: wide_rows lists their rows (every row of each such block)
 void launch_dedisp_direct(const DedispLaunch& p, bool u8, const void* rows, void* out,
                           const uint32_t* wide_rows, uint32_t nwide, cudaStream_t st);
+// RFI-masked 8-bit chunks (dedisp_h16.cu).  Transposes with bad channels / bad rows
+// zeroed, to u8 rows (integer path) or fp16 rows (the fp16 in-order kernel)
+void launch_transpose_masked(const uint8_t* in, uint64_t length, uint32_t nchans, const uint8_t* chan_bad,
+                             const uint8_t* samp_bad, void* rows, uint64_t pitch, bool h16, cudaStream_t st);
+// fp16 in-order kernel: staging table (p.wmax = halves per copy), launch, geometry
+constexpr int HX_CAP = 16;  // flagged rows per staged channel window (host-checked)
+void launch_ddh_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st);
+void launch_dedisp_h16(const DedispLaunch& p, const uint16_t* rows, float* out, cudaStream_t st);
+// widest stage that fits for a window of wmax halves per copy (0: none)
+int dedisp_h16_stage_width(uint32_t wmax);
 // warp-specialized TMA variant (dedisp_tma.cu); p.wmax (bytes) must be a multiple of 256
 void launch_dedisp_u8_ws(const DedispLaunch& p, int nslot, const uint8_t* rows, int32_t* out,
                          cudaStream_t st);
@@ -251,11 +267,24 @@ struct RfiParams {
 };
 struct RfiWork {
     DevBuf chan_bad, samp_bad, dbl, tmp, rows;
+    DevBuf xcnt, xP, xR, xF;  // fp16 path exceptions: bad-row prefix counts, ascending rows, values
 };
 // Flags and masks the time-major chunk x[n][nch] into `out` (float, same layout).
 template <typename T>
 void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w,
                     float* out, cudaStream_t st, uint64_t* n_bad_ch, uint64_t* n_bad_s);
+// the two halves of rfi_clean_impl: flags (w.chan_bad, w.samp_bad and their counts), then the
+// widened masked chunk
+template <typename T>
+void rfi_flags_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w, cudaStream_t st,
+                    uint64_t* n_bad_ch, uint64_t* n_bad_s);
+template <typename T>
+void rfi_mask_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w, float* out,
+                   cudaStream_t st, uint64_t nbc, uint64_t nrows_bad);
+// after rfi_flags_impl on an 8-bit chunk: w.xP[r] = bad rows < r (r <= n), w.xR = the nbad bad
+// rows ascending, w.xF[k][c] = apply_mask's value of cell (xR[k], c); rows_host gets xR
+void rfi_exceptions_u8(const uint8_t* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w,
+                       uint64_t nbad, cudaStream_t st, std::vector<uint32_t>* rows_host);
 
 // clustering
 struct ClusterWork;  // device scratch, defined in cluster.cu

@@ -258,6 +258,27 @@ __global__ void widen_kernel(const T* __restrict__ x, size_t cells, float* __res
         out[i] = (float)x[i];
 }
 
+// apply_mask's replacement of cell (i, c) of a bad row (src/rfi.cpp:115-136): the local
+// mean of the channel's unflagged cells within +-32 rows (double sum in row order), 0 for a
+// bad channel or under the zero policy
+template <typename T>
+__device__ __forceinline__ float mask_value(const T* __restrict__ x, uint64_t n, uint32_t nch,
+                                            const uint8_t* __restrict__ chan_bad,
+                                            const uint8_t* __restrict__ samp_bad, uint64_t i, uint32_t c,
+                                            int local_mean) {
+    if (!local_mean || chan_bad[c]) return 0.0f;
+    const uint64_t lo = i > 32 ? i - 32 : 0;
+    const uint64_t hi = min(n, i + 33);
+    double sum = 0.0;
+    uint64_t count = 0;
+    for (uint64_t j = lo; j < hi; ++j) {
+        if (samp_bad[j]) continue;
+        sum = __dadd_rn(sum, (double)(float)x[j * nch + c]);
+        ++count;
+    }
+    return count ? __double2float_rn(__ddiv_rn(sum, (double)count)) : 0.0f;
+}
+
 // masked cells of bad samples (rows) and bad channels (columns)
 template <typename T>
 __global__ void mask_kernel(const T* __restrict__ x, uint64_t n, uint32_t nch,
@@ -268,23 +289,71 @@ __global__ void mask_kernel(const T* __restrict__ x, uint64_t n, uint32_t nch,
     const uint64_t k = blockIdx.x;
     if (k < nbad_rows) {
         const uint64_t i = bad_rows[k];
-        for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x) {
-            float rep = 0.0f;
-            if (local_mean && !chan_bad[c]) {  // src/rfi.cpp:122-136
-                const uint64_t lo = i > 32 ? i - 32 : 0;
-                const uint64_t hi = min(n, i + 33);
-                double sum = 0.0;
-                uint64_t count = 0;
-                for (uint64_t j = lo; j < hi; ++j) {
-                    if (samp_bad[j]) continue;
-                    sum = __dadd_rn(sum, (double)(float)x[j * nch + c]);
-                    ++count;
-                }
-                rep = count ? __double2float_rn(__ddiv_rn(sum, (double)count)) : 0.0f;
-            }
-            out[i * nch + c] = rep;
-        }
+        for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x)
+            out[i * nch + c] = mask_value(x, n, nch, chan_bad, samp_bad, i, c, local_mean);
     }
+}
+
+// exceptions of the fp16 dedispersion path: value of every cell of the k-th bad row (rows
+// in ascending order), F[k][c]
+__global__ void mask_values_kernel(const uint8_t* __restrict__ x, uint64_t n, uint32_t nch,
+                                   const uint8_t* __restrict__ chan_bad, const uint8_t* __restrict__ samp_bad,
+                                   const uint32_t* __restrict__ rows, int local_mean, float* __restrict__ F) {
+    const uint64_t k = blockIdx.x;
+    const uint64_t i = rows[k];
+    for (uint32_t c = threadIdx.x; c < nch; c += blockDim.x)
+        F[k * nch + c] = mask_value(x, n, nch, chan_bad, samp_bad, i, c, local_mean);
+}
+
+// P[r] = number of bad rows < r (r <= n) and the ascending bad-row list R[P[r]] = r, in
+// blocks of 1024 rows: counts, one-CTA scan of the counts, per-block ballot scan
+constexpr int XR_ROWS = 1024;
+
+__global__ void __launch_bounds__(XR_ROWS) flag_counts_kernel(const uint8_t* __restrict__ bad, uint64_t n,
+                                                              uint32_t* __restrict__ cnt) {
+    const uint64_t r = (uint64_t)blockIdx.x * XR_ROWS + threadIdx.x;
+    const int f = r < n && bad[r];
+    const int c = __syncthreads_count(f);
+    if (threadIdx.x == 0) cnt[blockIdx.x] = (uint32_t)c;
+}
+
+__global__ void __launch_bounds__(1024) flag_scan_kernel(uint32_t* __restrict__ cnt, uint32_t nb) {
+    __shared__ uint32_t part[1024];
+    const uint32_t per = (nb + 1023) / 1024;
+    const uint32_t b0 = threadIdx.x * per, b1 = min(nb, b0 + per);
+    uint32_t s = 0;
+    for (uint32_t b = b0; b < b1; ++b) s += cnt[b];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    for (int o = 1; o < 1024; o <<= 1) {  // inclusive Hillis-Steele scan of the thread sums
+        const uint32_t v = threadIdx.x >= (unsigned)o ? part[threadIdx.x - o] : 0u;
+        __syncthreads();
+        part[threadIdx.x] += v;
+        __syncthreads();
+    }
+    uint32_t run = part[threadIdx.x] - s;  // exclusive
+    for (uint32_t b = b0; b < b1; ++b) {
+        const uint32_t v = cnt[b];
+        cnt[b] = run;
+        run += v;
+    }
+}
+
+__global__ void __launch_bounds__(XR_ROWS) flag_rows_kernel(const uint8_t* __restrict__ bad, uint64_t n,
+                                                            const uint32_t* __restrict__ base,
+                                                            uint32_t* __restrict__ P, uint32_t* __restrict__ R) {
+    __shared__ uint32_t wsum[XR_ROWS / 32];
+    const uint64_t r = (uint64_t)blockIdx.x * XR_ROWS + threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const bool f = r < n && bad[r];
+    const uint32_t m = __ballot_sync(0xffffffffu, f);
+    if (lane == 0) wsum[warp] = __popc(m);
+    __syncthreads();
+    uint32_t before = 0;
+    for (int w = 0; w < warp; ++w) before += wsum[w];
+    const uint32_t p = base[blockIdx.x] + before + __popc(m & ((1u << lane) - 1u));
+    if (r <= n) P[r] = p;
+    if (f) R[p] = (uint32_t)r;
 }
 
 __global__ void zero_channels_kernel(uint64_t n, uint32_t nch, const uint8_t* __restrict__ chan_bad,
@@ -322,9 +391,8 @@ void median_mad(const double* v, uint64_t n, double* st2, DevBuf& tmp, double* s
 }  // namespace
 
 template <typename T>
-void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w,
-                    float* out, cudaStream_t st, uint64_t* n_bad_ch, uint64_t* n_bad_s) {
-    const size_t cells = (size_t)n * nch;
+void rfi_flags_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w, cudaStream_t st,
+                    uint64_t* n_bad_ch, uint64_t* n_bad_s) {
     w.chan_bad.reserve(nch);
     w.samp_bad.reserve(n);
     PGB_CUDA(cudaMemsetAsync(w.chan_bad.p, 0, nch, st));
@@ -386,6 +454,12 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
     for (auto v : cb) nbc += v;
     *n_bad_ch = nbc;
     *n_bad_s = nrows_bad;
+}
+
+template <typename T>
+void rfi_mask_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w, float* out,
+                   cudaStream_t st, uint64_t nbc, uint64_t nrows_bad) {
+    const size_t cells = (size_t)n * nch;
     const bool rows4 = nch % 4 == 0 && !pgb_ablation_env("PGB_RFI_SERIAL");
     if (rows4)  // bad channels zeroed while widening
         widen_rows_kernel<T><<<148 * 16, 256, 0, st>>>(x, n, nch, w.chan_bad.as<uint8_t>(), out);
@@ -405,9 +479,45 @@ void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, R
     PGB_CUDA(cudaGetLastError());
 }
 
+template <typename T>
+void rfi_clean_impl(const T* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w,
+                    float* out, cudaStream_t st, uint64_t* n_bad_ch, uint64_t* n_bad_s) {
+    rfi_flags_impl(x, n, nch, rp, w, st, n_bad_ch, n_bad_s);
+    rfi_mask_impl(x, n, nch, rp, w, out, st, *n_bad_ch, *n_bad_s);
+}
+
+void rfi_exceptions_u8(const uint8_t* x, uint64_t n, uint32_t nch, const RfiParams& rp, RfiWork& w,
+                       uint64_t nbad, cudaStream_t st, std::vector<uint32_t>* rows_host) {
+    if (n >= (1ull << 32)) raise(PGB_ERR_CONFIG, "chunk longer than 2^32 samples");
+    const uint32_t nb = (uint32_t)((n + 1 + XR_ROWS - 1) / XR_ROWS);  // rows 0 .. n (P[n] = total)
+    w.xcnt.reserve(sizeof(uint32_t) * nb);
+    w.xP.reserve(sizeof(uint32_t) * (n + 1));
+    w.xR.reserve(sizeof(uint32_t) * std::max<uint64_t>(nbad, 1));
+    w.xF.reserve(sizeof(float) * std::max<uint64_t>(nbad, 1) * nch);
+    const uint8_t* bad = w.samp_bad.as<uint8_t>();
+    flag_counts_kernel<<<nb, XR_ROWS, 0, st>>>(bad, n, w.xcnt.as<uint32_t>());
+    flag_scan_kernel<<<1, 1024, 0, st>>>(w.xcnt.as<uint32_t>(), nb);
+    flag_rows_kernel<<<nb, XR_ROWS, 0, st>>>(bad, n, w.xcnt.as<uint32_t>(), w.xP.as<uint32_t>(),
+                                             w.xR.as<uint32_t>());
+    if (nbad)
+        mask_values_kernel<<<(unsigned)nbad, 256, 0, st>>>(x, n, nch, w.chan_bad.as<uint8_t>(), bad,
+                                                           w.xR.as<uint32_t>(), rp.local_mean, w.xF.as<float>());
+    PGB_CUDA(cudaGetLastError());
+    if (rows_host) {
+        rows_host->resize(nbad);
+        if (nbad)
+            PGB_CUDA(cudaMemcpyAsync(rows_host->data(), w.xR.p, nbad * sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+        PGB_CUDA(cudaStreamSynchronize(st));
+    }
+}
+
 template void rfi_clean_impl<uint8_t>(const uint8_t*, uint64_t, uint32_t, const RfiParams&, RfiWork&,
                                       float*, cudaStream_t, uint64_t*, uint64_t*);
-template void rfi_clean_impl<float>(const float*, uint64_t, uint32_t, const RfiParams&, RfiWork&,
-                                    float*, cudaStream_t, uint64_t*, uint64_t*);
+template void rfi_clean_impl<float>(const float*, uint64_t, uint32_t, const RfiParams&, RfiWork&, float*,
+                                    cudaStream_t, uint64_t*, uint64_t*);
+template void rfi_flags_impl<uint8_t>(const uint8_t*, uint64_t, uint32_t, const RfiParams&, RfiWork&,
+                                      cudaStream_t, uint64_t*, uint64_t*);
+template void rfi_mask_impl<uint8_t>(const uint8_t*, uint64_t, uint32_t, const RfiParams&, RfiWork&, float*,
+                                     cudaStream_t, uint64_t, uint64_t);
 
 }  // namespace pgb
