@@ -167,6 +167,7 @@ struct pgb_context {
     DevBuf cl_scratch, clusters, members;
     DevBuf d_wide;    // rows of trial blocks too wide for the staged dedispersion
     DevBuf d_levels;  // boxcar ladder levels above the tile kernel's (boxcar_max > 8192)
+    DevBuf d_bxs;     // boxcar launcher scratch
     PinnedBuf h_counters;
     RfiWork rfi;
     DevBuf rfi_out;
@@ -800,6 +801,12 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     run.work = work;
 }
 
+// The boxcar launcher's tile list (tiles the prefix kernel hands to the tree kernel).
+void* box_scratch(pgb_context* ctx, uint32_t nrows, uint64_t max_len, uint64_t boxcar_max) {
+    ctx->d_bxs.reserve(boxcar_scratch_bytes(nrows, max_len, boxcar_max));
+    return ctx->d_bxs.p;
+}
+
 // Global ladder levels for boxcar_max > BX_TILE_MAX (null otherwise).
 double* box_levels(pgb_context* ctx, uint64_t boxcar_max, uint32_t nrows, uint64_t pitch) {
     const size_t b = boxcar_levels_bytes(boxcar_max, nrows, pitch);
@@ -850,7 +857,8 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
                             ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
                             ctx->d_scale.as<double>(), ctx->cands_raw.as<pgb_candidate>(), dcnt,
                             ctx->cand_cap, ctx->frags.as<Fragment>(), dcnt + 1, ctx->frag_cap,
-                            box_levels(ctx, cfg->boxcar_max, nrows, out_pitch), st);
+                            box_levels(ctx, cfg->boxcar_max, nrows, out_pitch),
+                            box_scratch(ctx, nrows, max_n, cfg->boxcar_max), st);
         PGB_CUDA(cudaEventRecord(ctx->ev_bx1, st));
         PGB_CUDA(cudaMemcpyAsync(hcnt, dcnt, 2 * sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
         PGB_CUDA(cudaStreamSynchronize(st));
@@ -967,7 +975,8 @@ void chunk_back_async(pgb_context* ctx, ChunkRun& run, uint8_t* h_status, uint64
                         ctx->slot_active[slot].as<uint32_t>(), ctx->d_dms.as<double>(),
                         ctx->d_scale.as<double>(), ctx->cands_raw.as<pgb_candidate>(), dcnt, ccap,
                         ctx->frags.as<Fragment>(), dcnt + 1, fcap,
-                        box_levels(ctx, cfg->boxcar_max, run.nrows, run.out_pitch), st);
+                        box_levels(ctx, cfg->boxcar_max, run.nrows, run.out_pitch),
+                        box_scratch(ctx, run.nrows, run.max_n, cfg->boxcar_max), st);
     trace_mark(ctx, "boxcar + runs", st);
     sort_fragments_dev(ctx->frags.as<Fragment>(), ctx->frags_sorted.as<Fragment>(), fcap, dcnt + 1,
                        ctx->sort_tmp.p, tmp, ka, ka + cap, ia, ia + cap, st);

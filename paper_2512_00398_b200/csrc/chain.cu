@@ -26,6 +26,10 @@
 
 #include <cooperative_groups.h>
 
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+
 #include "pgb_internal.h"
 
 namespace cg = cooperative_groups;
@@ -740,22 +744,21 @@ __device__ __forceinline__ void ladder_regs(double (&r)[S]) {
 }
 
 template <int KIND, int S>
-__global__ void __launch_bounds__(BX_THREADS)
-    boxcar_peaks_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len,
-                        const float* __restrict__ frms_all, const uint8_t* __restrict__ status,
-                        uint64_t pitch, uint64_t bmax, const double* __restrict__ scale,
-                        PeakCtx ctx, double* __restrict__ lvl_out) {
+__device__ __forceinline__ void boxcar_tile(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len,
+                                            const float* __restrict__ frms_all, const uint8_t* __restrict__ status,
+                                            uint64_t pitch, uint64_t bmax, const double* __restrict__ scale,
+                                            const PeakCtx& ctx, double* __restrict__ lvl_out, const uint32_t row,
+                                            const uint32_t tile) {
     constexpr int N = BX_THREADS * S;
     // S == 16 (boxcar_max <= 4096): each buffer carries a zero pad of N/4 >= max half so
     // the shifted read needs no bounds test; S == 24 (8192) tests instead (smem limit).
     constexpr bool kPad = S == 16;
     constexpr uint32_t LD = kPad ? N + N / 4 : N;
     extern __shared__ double sbuf[];  // ping-pong [2][LD]
-    const uint32_t row = blockIdx.x;  // rows on x: more than 65535 trials are legal
     if (status[row]) return;
     const uint64_t n = row_len[row];
     const uint32_t T = N - (uint32_t)bmax;
-    const uint64_t i0 = (uint64_t)blockIdx.y * T;
+    const uint64_t i0 = (uint64_t)tile * T;
     if (i0 >= n) return;
     const float frms = frms_all[row];
     const int tid = threadIdx.x;
@@ -890,6 +893,278 @@ __global__ void __launch_bounds__(BX_THREADS)
         for (int k = 0; k < S; ++k) {
             const uint32_t j = tid + BX_THREADS * k;
             if (j < lim2) dst[j] = r[k];
+        }
+    }
+}
+
+// The reference's doubling tree level by level in shared memory (src/detect.cpp:216-221),
+// for every (row, tile) of the grid, or -- list mode -- for the tiles the prefix kernel
+// could not prove exact.
+template <int KIND, int S>
+__global__ void __launch_bounds__(BX_THREADS)
+    boxcar_peaks_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len,
+                        const float* __restrict__ frms_all, const uint8_t* __restrict__ status,
+                        uint64_t pitch, uint64_t bmax, const double* __restrict__ scale,
+                        PeakCtx ctx, double* __restrict__ lvl_out, const uint2* __restrict__ list,
+                        const unsigned* __restrict__ nlist) {
+    if (!list) {
+        boxcar_tile<KIND, S>(x_all, row_len, frms_all, status, pitch, bmax, scale, ctx, lvl_out, blockIdx.x,
+                             blockIdx.y);  // rows on x: more than 65535 trials are legal
+        return;
+    }
+    const unsigned cnt = *nlist;
+    for (unsigned i = blockIdx.x; i < cnt; i += gridDim.x) {
+        const uint2 t = list[i];
+        boxcar_tile<KIND, S>(x_all, row_len, frms_all, status, pitch, bmax, scale, ctx, lvl_out, t.x, t.y);
+        __syncthreads();  // the next tile reuses the shared buffers
+    }
+}
+
+// ---- prefix-sum boxcar ------------------------------------------------------------
+// The tree sums of a level are sums of contiguous ranges of s = double(x / rms).  If every
+// s of a tile is a multiple of 2^L and every prefix sum of the tile is below 2^51 * 2^L in
+// magnitude, each partial sum the tree forms (a range sum, |.| < 2^52 * 2^L) is exactly
+// representable, so every level value IS the exact range sum P[j + w] - P[j] of the
+// tile's prefix sums -- which are then exact in double as well.  The kernel checks that per
+// tile (the values are floats, so it holds unless a tile mixes magnitudes ~2^24 apart;
+// a rounded prefix sum would show up as |P| >= 2^51 * 2^L), then tests each level as one DADD +
+// DSETP against an exact cut (fl(d * sc) > thr <=> d > cut_w, d a multiple of 2^L): no
+// level-to-level dependency, no barrier or shared-memory write per level.  Levels w >= 8
+// first bound a whole strip -- max P over its partners' strips minus min P over its own
+// outputs -- and compute the strip only when the bound reaches the cut (rare for noise).
+// Runs are scanned per thread strip, as in the tree kernel, only for the levels some
+// element exceeds; tiles that fail the check go to boxcar_peaks_kernel (list mode).
+__device__ __forceinline__ uint32_t XP(uint32_t j) { return j + (j >> 5); }
+
+template <int KIND, int S>
+__global__ void __launch_bounds__(BX_THREADS)
+    boxcar_prefix_kernel(const void* __restrict__ x_all, const uint32_t* __restrict__ row_len,
+                         const float* __restrict__ frms_all, const uint8_t* __restrict__ status,
+                         uint64_t pitch, uint64_t bmax, const double* __restrict__ scale, PeakCtx ctx,
+                         double* __restrict__ lvl_out, uint2* __restrict__ fb_list, unsigned* __restrict__ fb_n) {
+    constexpr int N = BX_THREADS * S;
+    constexpr int NW = BX_THREADS / 32;
+    extern __shared__ __align__(16) uint8_t bsm[];
+    // shared arrays padded by one element per 32 (XP): the strip accesses of a warp (stride
+    // S elements) spread over the banks instead of hitting 2-8 of them
+    double* P = reinterpret_cast<double*>(bsm);                     // [XP(N) + 1]: P[XP(j)] = sum s[0..j)
+    float* xs = reinterpret_cast<float*>(P + XP(N) + 2);            // [XP(N)] the tile's inputs
+    __shared__ double s_tot[NW], s_amax[NW], s_cut[32];
+    __shared__ double s_smax[BX_THREADS + 2], s_smin[BX_THREADS + 2];  // per strip extremes of P
+    __shared__ float s_fmax[NW], s_fmin[NW];
+    __shared__ unsigned s_mask;
+    const uint32_t row = blockIdx.x, tile = blockIdx.y;
+    if (status[row]) return;
+    const uint64_t n = row_len[row];
+    const uint32_t T = N - (uint32_t)bmax;
+    const uint64_t i0 = (uint64_t)tile * T;
+    if (i0 >= n) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const float frms = frms_all[row];
+    const uint32_t nin = (uint32_t)(n - i0 < (uint64_t)N ? n - i0 : (uint64_t)N);
+    const size_t base = (size_t)row * pitch + i0;
+    // coalesced loads, staged so each thread can take a contiguous strip
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+        const uint32_t j = tid + BX_THREADS * k;
+        xs[XP(j)] = j < nin ? load_x<KIND>(x_all, base + j) : 0.0f;
+    }
+    if (tid == 0) s_mask = 0;
+    __syncthreads();
+    // strip [S*tid, S*tid + S): the reference's float quotients (:211), strip prefix in double
+    const uint32_t j0 = (uint32_t)S * tid;
+    double ps[S + 1];  // ps[k] = P[j0 + k]
+    ps[0] = 0.0;
+    float fhi = 0.0f, flo = INFINITY;  // largest |s| and smallest nonzero |s|
+#pragma unroll
+    for (int k = 0; k < S; ++k) {
+        const float f = j0 + k < nin ? __fdiv_rn(xs[XP(j0 + k)], frms) : 0.0f;
+        const float af = fabsf(f);
+        fhi = fmaxf(fhi, af);
+        flo = fminf(flo, af > 0.0f ? af : INFINITY);
+        ps[k + 1] = __dadd_rn(ps[k], (double)f);
+    }
+    // block exclusive scan of the strip totals (exact when the tile passes the check)
+    double tot = ps[S];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double v = __shfl_up_sync(0xffffffffu, tot, o);
+        if (lane >= o) tot = __dadd_rn(tot, v);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        fhi = fmaxf(fhi, __shfl_xor_sync(0xffffffffu, fhi, o));
+        flo = fminf(flo, __shfl_xor_sync(0xffffffffu, flo, o));
+    }
+    if (lane == 31) s_tot[warp] = tot;
+    if (lane == 0) {
+        s_fmax[warp] = fhi;
+        s_fmin[warp] = flo;
+    }
+    __syncthreads();
+    double off = __dsub_rn(tot, ps[S]);  // exclusive within the warp
+    for (int w = 0; w < warp; ++w) off = __dadd_rn(off, s_tot[w]);
+    fhi = s_fmax[0];
+    flo = s_fmin[0];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+        fhi = fmaxf(fhi, s_fmax[w]);
+        flo = fminf(flo, s_fmin[w]);
+    }
+    // L: the lsb exponent of the smallest nonzero |s| bounds every value's lsb from below
+    // (a float's lsb is 2^(e - 23), e its exponent, subnormals 2^-149)
+    int L = 0;
+    bool exact = !(fhi > 3.0e38f);  // inf / NaN: never exact
+    if (flo < INFINITY) {
+        const uint32_t be = __float_as_uint(flo) >> 23;
+        L = (be ? (int)be - 127 : -126) - 23;
+    }
+    double smx = -INFINITY, smn = INFINITY, amax = 0.0;
+    ps[0] = off;
+#pragma unroll
+    for (int k = 0; k <= S; ++k) {
+        if (k) ps[k] = __dadd_rn(ps[k], off);
+        if (k < S) {
+            P[XP(j0 + k)] = ps[k];
+            smx = fmax(smx, ps[k]);
+            smn = fmin(smn, ps[k]);
+        }
+        amax = fmax(amax, fabs(ps[k]));
+    }
+    if (tid == BX_THREADS - 1) {  // P[N], then pseudo-strips past the tile
+        P[XP(N)] = ps[S];
+        s_smax[BX_THREADS] = s_smin[BX_THREADS] = ps[S];
+        s_smax[BX_THREADS + 1] = -INFINITY;
+        s_smin[BX_THREADS + 1] = INFINITY;
+    }
+    s_smax[tid] = smx;
+    s_smin[tid] = smn;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) amax = fmax(amax, __shfl_xor_sync(0xffffffffu, amax, o));
+    if (lane == 0) s_amax[warp] = amax;
+    // exact per-level cuts: cut_w = C 2^L with C the largest integer such that
+    // fl(C 2^L sc_w) <= thr (monotone), so a multiple d of 2^L passes iff d > cut_w
+    uint32_t nlev = 0;
+    for (uint64_t w = 1; w <= bmax && w <= n; w <<= 1) ++nlev;
+    const double thr = ctx.cp.threshold;
+    const double p2l = ldexp(1.0, max(L, -1074)), p2nl = ldexp(1.0, min(-L, 1023));
+    if (warp == 0 && (uint32_t)lane < nlev) {
+        const double sc = scale[lane];
+        const double lim = 9007199254740992.0;  // 2^53
+        const double c0 = floor(__dmul_rn(thr / sc, p2nl));
+        double c;
+        if (!(c0 < lim)) c = lim;              // no level value reaches it
+        else if (!(c0 > -lim)) c = -lim - 1.0;  // every level value passes
+        else {
+            c = c0;
+            while (c + 1.0 < lim && !(__dmul_rn(__dmul_rn(c + 1.0, p2l), sc) > thr)) c += 1.0;
+            while (c > -lim && __dmul_rn(__dmul_rn(c, p2l), sc) > thr) c -= 1.0;
+        }
+        s_cut[lane] = __dmul_rn(c, p2l);
+    }
+    __syncthreads();
+    amax = s_amax[0];
+#pragma unroll
+    for (int w = 1; w < NW; ++w) amax = fmax(amax, s_amax[w]);
+    // every value a multiple of 2^L (normal range), every prefix sum below 2^51 * 2^L: every
+    // range sum (tree partial sums, the scan's partial totals) is then below 2^52 * 2^L, i.e.
+    // representable, and a rounded one could not have hidden below the bound
+    exact = exact && L >= -1000 && L <= 1000 && amax < ldexp(1.0, 51 + L);
+    if (!exact) {  // block-uniform: the tree kernel takes this tile
+        if (tid == 0) fb_list[atomicAdd(fb_n, 1u)] = make_uint2(row, tile);
+        return;
+    }
+    // levels w <= 4: every output of the strip, d = P[j + w] - P[j] from the strip's registers
+    // (partners past the strip from shared memory)
+    uint32_t level = 0;
+#pragma unroll
+    for (int l = 0; l < 3; ++l) {
+        const uint32_t w = 1u << l;
+        if (w > bmax || w > n) continue;  // (levels stop at the first such w)
+        const uint64_t m = n - w + 1;
+        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+        const double cut = s_cut[l];
+        int any = 0;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const double hi = k + (int)w <= S ? ps[k + (int)w <= S ? k + w : 0] : P[XP(min(j0 + k + w, (uint32_t)N))];
+            any |= (j0 + k < lim2) & (__dsub_rn(hi, ps[k]) > cut);
+        }
+        if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&s_mask, 1u << l);
+        level = l + 1;
+    }
+    // levels w >= 8: a strip can hold an output above the cut only if max P over the strips
+    // covering its partners [j0 + w, j0 + w + S) minus min P over its own outputs exceeds it
+    for (uint64_t w = 8; w <= bmax && w <= n && level < 32; w <<= 1, ++level) {
+        const uint64_t m = n - w + 1;
+        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+        const double cut = s_cut[level];
+        const uint32_t q = (uint32_t)w / S;
+        const uint32_t a = min((uint32_t)tid + q, (uint32_t)BX_THREADS + 1);
+        const uint32_t b = min((uint32_t)tid + q + 1, (uint32_t)BX_THREADS + 1);
+        int any = 0;
+        if (j0 < lim2 && __dsub_rn(fmax(s_smax[a], s_smax[b]), s_smin[tid]) > cut) {
+#pragma unroll
+            for (int k = 0; k < S; ++k)
+                any |= (j0 + k < lim2) & (__dsub_rn(P[XP(min(j0 + k + (uint32_t)w, (uint32_t)N))], ps[k]) > cut);
+        }
+        if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&s_mask, 1u << level);
+    }
+    __syncthreads();
+    const unsigned mask = s_mask;
+    // threshold runs of the flagged levels on contiguous strips, as the tree kernel
+    level = 0;
+    for (uint64_t w = 1; w <= bmax && w <= n; w <<= 1, ++level) {
+        const uint64_t m = n - w + 1;
+        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+        if (mask & (1u << level)) {
+            const double sc = scale[level];
+            const uint32_t lo = j0;
+            const uint32_t hi = min(lo + S, lim2);
+            bool in_run = false;
+            uint32_t rb = 0, pk = 0;
+            double pv = 0.0;
+            for (uint32_t j = lo; j < hi; ++j) {
+                // the exact level sum times 1/sqrt(w) (:219)
+                const double v = __dmul_rn(__dsub_rn(P[XP(j + (uint32_t)w)], P[XP(j)]), sc);
+                if (v > thr) {
+                    if (!in_run) {
+                        in_run = true;
+                        rb = j;
+                        pk = j;
+                        pv = v;
+                    } else if (v > pv) {
+                        pk = j;
+                        pv = v;
+                    }
+                } else if (in_run) {
+                    in_run = false;
+                    const bool left_open = rb == lo && i0 + lo > 0;
+                    if (left_open)
+                        emit_fragment(ctx, row, level, i0 + rb, i0 + j - 1, i0 + pk, pv);
+                    else
+                        emit_candidate(ctx, row, level, m, i0 + rb, i0 + j - 1, i0 + pk, pv);
+                }
+            }
+            if (in_run) {
+                const bool left_open = rb == lo && i0 + lo > 0;
+                const bool right_open = i0 + hi < m;
+                if (left_open || right_open)
+                    emit_fragment(ctx, row, level, i0 + rb, i0 + hi - 1, i0 + pk, pv);
+                else
+                    emit_candidate(ctx, row, level, m, i0 + rb, i0 + hi - 1, i0 + pk, pv);
+            }
+        }
+    }
+    // boxcar_max beyond the tile ladder: the top level's exact values for the level kernel
+    if (lvl_out && n >= bmax) {
+        const uint64_t m = n - bmax + 1;
+        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+        double* dst = lvl_out + base;
+#pragma unroll
+        for (int k = 0; k < S; ++k) {
+            const uint32_t j = tid + BX_THREADS * k;
+            if (j < lim2) dst[j] = __dsub_rn(P[XP(j + (uint32_t)bmax)], P[XP(j)]);
         }
     }
 }
@@ -1046,7 +1321,7 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
                          const ChainParams& cp, const uint32_t* active, const double* dms,
                          const double* scale, pgb_candidate* cands, unsigned long long* n_cands,
                          uint64_t cand_cap, Fragment* frags, unsigned long long* n_frags,
-                         uint64_t frag_cap, double* levels, cudaStream_t st) {
+                         uint64_t frag_cap, double* levels, void* scratch, cudaStream_t st) {
     if (!nrows || !max_len) return;
     PeakCtx ctx{active, dms, cp, cands, n_cands, cand_cap, frags, n_frags, frag_cap};
     // boxcar_max > BX_TILE_MAX: the tile kernel runs the ladder to w = BX_TILE_LADDER and
@@ -1064,12 +1339,47 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
     const unsigned tiles = (unsigned)((max_len + T - 1) / T);
     const size_t smem = 2 * LD * sizeof(double);
     dim3 grid(nrows, tiles);
+    // default: the prefix-sum kernel, then the tree kernel for the tiles it could not prove
+    // exact (list mode, a device-side count); PGB_BOXCAR_TREE=1: the tree kernel everywhere
+    const bool tree = pgb_ablation_env("PGB_BOXCAR_TREE") != nullptr;
+    uint2* fb_list = reinterpret_cast<uint2*>(static_cast<char*>(scratch) + 16);
+    unsigned* fb_n = static_cast<unsigned*>(scratch);
+    if (!tree) {
+        PGB_CUDA(cudaMemsetAsync(fb_n, 0, sizeof(unsigned), st));
+        const size_t psm = (N + N / 32 + 2) * sizeof(double) + (N + N / 32) * sizeof(float);
+#define PGB_BXP(K, SS)                                                                        \
+    do {                                                                                      \
+        PGB_CUDA(cudaFuncSetAttribute(boxcar_prefix_kernel<K, SS>,                            \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)psm)); \
+        boxcar_prefix_kernel<K, SS><<<grid, BX_THREADS, psm, st>>>(x, row_len, frms, status, pitch, bmax, \
+                                                                   scale, ctx, lvl_out, fb_list, fb_n); \
+    } while (0)
+        if (S == 16) {
+            if (kind == 1) PGB_BXP(1, 16);
+            else PGB_BXP(0, 16);
+        } else {
+            if (kind == 1) PGB_BXP(1, 24);
+            else PGB_BXP(0, 24);
+        }
+#undef PGB_BXP
+        PGB_CUDA(cudaGetLastError());
+    }
+    static const bool which = getenv("PGB_DD_WHICH") != nullptr;  // kernel-choice log (tests)
+    if (which && !tree) {
+        unsigned nfb = 0;
+        PGB_CUDA(cudaMemcpyAsync(&nfb, fb_n, sizeof nfb, cudaMemcpyDeviceToHost, st));
+        PGB_CUDA(cudaStreamSynchronize(st));
+        fprintf(stderr, "pgb boxcar: prefix kernel, %u of %llu tiles to the tree kernel\n", nfb,
+                (unsigned long long)nrows * tiles);
+    }
+    const dim3 tgrid = tree ? grid : dim3(148 * 2);
+    const uint2* lst = tree ? nullptr : fb_list;
 #define PGB_BX(K, SS)                                                                        \
     do {                                                                                     \
         PGB_CUDA(cudaFuncSetAttribute(boxcar_peaks_kernel<K, SS>,                            \
                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)); \
-        boxcar_peaks_kernel<K, SS><<<grid, BX_THREADS, smem, st>>>(x, row_len, frms, status, \
-                                                                   pitch, bmax, scale, ctx, lvl_out); \
+        boxcar_peaks_kernel<K, SS><<<tgrid, BX_THREADS, smem, st>>>(x, row_len, frms, status, \
+                                                                    pitch, bmax, scale, ctx, lvl_out, lst, fb_n); \
     } while (0)
     if (S == 16) {
         if (kind == 1) PGB_BX(1, 16);
@@ -1095,6 +1405,12 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
             std::swap(in, out);
         }
     }
+}
+
+size_t boxcar_scratch_bytes(uint32_t nrows, uint64_t max_len, uint64_t boxcar_max) {
+    const uint64_t bmax = boxcar_max > BX_TILE_MAX ? BX_TILE_LADDER : boxcar_max;
+    const uint64_t T = (uint64_t)BX_THREADS * (bmax <= 2048 ? 16 : 24) - bmax;
+    return 16 + (size_t)nrows * ((max_len + T - 1) / T) * sizeof(uint2);
 }
 
 size_t boxcar_levels_bytes(uint64_t boxcar_max, uint32_t nrows, uint64_t pitch) {

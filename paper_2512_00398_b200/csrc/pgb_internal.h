@@ -218,7 +218,9 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
                          uint64_t max_len, const ChainParams& cp, const uint32_t* active,
                          const double* dms, const double* scale, pgb_candidate* cands, unsigned long long* n_cands,
                          uint64_t cand_cap, Fragment* frags, unsigned long long* n_frags,
-                         uint64_t frag_cap, double* levels, cudaStream_t st);
+                         uint64_t frag_cap, double* levels, void* scratch, cudaStream_t st);
+// device scratch of launch_boxcar_peaks (the tree kernel's tile list)
+size_t boxcar_scratch_bytes(uint32_t nrows, uint64_t max_len, uint64_t boxcar_max);
 void launch_stitch(const Fragment* frags_sorted, uint64_t nfrags, const uint32_t* row_len,
                    const ChainParams& cp, const uint32_t* active, const double* dms,
                    pgb_candidate* cands, unsigned long long* n_cands, uint64_t cand_cap,
