@@ -172,6 +172,50 @@ __global__ void __launch_bounds__(256)
     if (lane == 0) bs[(size_t)row * nb + b] = s;
 }
 
+// An interior warp segment of baseline_warp_kernel: 32-bit indices and differences
+// (|d| < 2^21, 128-sample prefix < 2^28), the window sum itself stays int64.  A lane owns 4
+// consecutive samples i4 .. i4+3 (i4 16-byte aligned) and needs x[i + h] and x[i - 1 - h]:
+// each set is 4 consecutive ints starting R = h mod 4 (resp. 3 - R) past an aligned
+// address, taken from two aligned 16-byte loads (the second mostly an L1 hit of the
+// neighbour lane's first) instead of eight 4-byte loads.
+template <int R>
+__device__ __forceinline__ void baseline_interior(const int32_t* __restrict__ x, float* __restrict__ out,
+                                                  int64_t s0, int64_t s1, uint32_t hh, long long carry,
+                                                  double inv_full, int lane) {
+    constexpr int RB = (3 - R) & 3;  // (-1 - h) mod 4
+    for (uint32_t base = (uint32_t)s0; base < (uint32_t)s1; base += 128) {
+        const uint32_t i4 = base + 4 * lane;
+        const int4 xq = *reinterpret_cast<const int4*>(x + i4);  // 16-byte aligned (pitch, base)
+        const int4* pa = reinterpret_cast<const int4*>(x + i4 + hh - R);
+        const int4* pb = reinterpret_cast<const int4*>(x + i4 - 1 - hh - RB);
+        const int4 a0 = pa[0], a1 = pa[1], b0 = pb[0], b1 = pb[1];
+        const int32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        const int32_t bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+        const int32_t xv[4] = {xq.x, xq.y, xq.z, xq.w};
+        int32_t d[4];
+        int32_t local = 0;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t i = i4 + k;
+            d[k] = (i > (uint32_t)s0 && i < (uint32_t)s1) ? av[R + k] - bv[RB + k] : 0;
+            local += d[k];
+        }
+        int32_t incl = local;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        long long run = carry + (long long)(incl - local);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            run += d[k];
+            if (i4 + k < (uint32_t)s1)
+                out[i4 + k] = __double2float_rn(__fma_rn(-(double)run, inv_full, (double)xv[k]));  // :45
+        }
+        carry += __shfl_sync(0xffffffffu, incl, 31);
+    }
+}
+
 __global__ void __launch_bounds__(256)
     baseline_warp_kernel(const int32_t* __restrict__ x_all, float* __restrict__ out_all,
                          const uint32_t* __restrict__ row_len, uint64_t pitch, uint64_t window,
@@ -209,36 +253,14 @@ __global__ void __launch_bounds__(256)
         for (int64_t i = lo + lane; i <= hi; i += 32) part += x[i];
     }
     long long carry = warp_sum_ll(part);  // S_{s0}; d_{s0} := 0 below
-    if (s0 >= h + 1 && s1 - 1 + h <= n - 1) {
-        // interior segment: every window is whole (one reciprocal), every x[i +- h] exists;
-        // 32-bit indices and differences (|d| < 2^21, 128-sample prefix < 2^28), the
-        // window sum itself stays int64
-        const uint32_t hh = (uint32_t)h;
-        for (uint32_t base = (uint32_t)s0; base < (uint32_t)s1; base += 128) {
-            const uint32_t i4 = base + 4 * lane;
-            const int4 xq = *reinterpret_cast<const int4*>(x + i4);  // 16-byte aligned (pitch, base)
-            const int32_t xv[4] = {xq.x, xq.y, xq.z, xq.w};
-            int32_t d[4];
-            int32_t local = 0;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const uint32_t i = i4 + k;
-                d[k] = (i > (uint32_t)s0 && i < (uint32_t)s1) ? x[i + hh] - x[i - 1 - hh] : 0;
-                local += d[k];
-            }
-            int32_t incl = local;
-            for (int o = 1; o < 32; o <<= 1) {
-                const int32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= o) incl += y;
-            }
-            long long run = carry + (long long)(incl - local);
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                run += d[k];
-                if (i4 + k < (uint32_t)s1)
-                    out[i4 + k] = __double2float_rn(__fma_rn(-(double)run, inv_full, (double)xv[k]));  // :45
-            }
-            carry += __shfl_sync(0xffffffffu, incl, 31);
+    if (s0 >= h + 4 && s1 - 1 + h <= n - 1 && (uint64_t)(s1 + h + 4) <= pitch) {
+        // interior segment: every window is whole (one reciprocal), every x[i +- h] exists,
+        // and the aligned 16-byte loads around them stay inside the row
+        switch (h & 3) {  // the partners' misalignment (warp-uniform): aligned 16-byte loads
+            case 0: baseline_interior<0>(x, out, s0, s1, (uint32_t)h, carry, inv_full, lane); break;
+            case 1: baseline_interior<1>(x, out, s0, s1, (uint32_t)h, carry, inv_full, lane); break;
+            case 2: baseline_interior<2>(x, out, s0, s1, (uint32_t)h, carry, inv_full, lane); break;
+            default: baseline_interior<3>(x, out, s0, s1, (uint32_t)h, carry, inv_full, lane); break;
         }
         return;
     }
@@ -955,19 +977,20 @@ __global__ void __launch_bounds__(BX_THREADS)
     __shared__ unsigned s_mask;
     const uint32_t row = blockIdx.x, tile = blockIdx.y;
     if (status[row]) return;
-    const uint64_t n = row_len[row];
+    const uint32_t n = row_len[row];  // series lengths and tile starts are 32-bit (row_len)
     const uint32_t T = N - (uint32_t)bmax;
-    const uint64_t i0 = (uint64_t)tile * T;
+    const uint32_t i0 = tile * T;
     if (i0 >= n) return;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const float frms = frms_all[row];
-    const uint32_t nin = (uint32_t)(n - i0 < (uint64_t)N ? n - i0 : (uint64_t)N);
+    const uint32_t nin = min(n - i0, (uint32_t)N);
     const size_t base = (size_t)row * pitch + i0;
     // coalesced loads, staged so each thread can take a contiguous strip
+    const uint32_t xp0 = XP(tid);  // XP(tid + 512 k) = XP(tid) + 528 k
 #pragma unroll
     for (int k = 0; k < S; ++k) {
         const uint32_t j = tid + BX_THREADS * k;
-        xs[XP(j)] = j < nin ? load_x<KIND>(x_all, base + j) : 0.0f;
+        xs[xp0 + (BX_THREADS + BX_THREADS / 32) * k] = j < nin ? load_x<KIND>(x_all, base + j) : 0.0f;
     }
     if (tid == 0) s_mask = 0;
     __syncthreads();
@@ -1019,18 +1042,19 @@ __global__ void __launch_bounds__(BX_THREADS)
         const uint32_t be = __float_as_uint(flo) >> 23;
         L = (be ? (int)be - 127 : -126) - 23;
     }
-    double smx = -INFINITY, smn = INFINITY, amax = 0.0;
     ps[0] = off;
+    double smx = off, smn = off;
 #pragma unroll
-    for (int k = 0; k <= S; ++k) {
-        if (k) ps[k] = __dadd_rn(ps[k], off);
+    for (int k = 1; k <= S; ++k) {
+        ps[k] = __dadd_rn(ps[k], off);
         if (k < S) {
-            P[XP(j0 + k)] = ps[k];
-            smx = fmax(smx, ps[k]);
-            smn = fmin(smn, ps[k]);
+            smx = ps[k] > smx ? ps[k] : smx;
+            smn = ps[k] < smn ? ps[k] : smn;
         }
-        amax = fmax(amax, fabs(ps[k]));
     }
+#pragma unroll
+    for (int k = 0; k < S; ++k) P[XP(j0 + k)] = ps[k];
+    double amax = fmax(fmax(fabs(smx), fabs(smn)), fabs(ps[S]));
     if (tid == BX_THREADS - 1) {  // P[N], then pseudo-strips past the tile
         P[XP(N)] = ps[S];
         s_smax[BX_THREADS] = s_smin[BX_THREADS] = ps[S];
@@ -1045,7 +1069,7 @@ __global__ void __launch_bounds__(BX_THREADS)
     // exact per-level cuts: cut_w = C 2^L with C the largest integer such that
     // fl(C 2^L sc_w) <= thr (monotone), so a multiple d of 2^L passes iff d > cut_w
     uint32_t nlev = 0;
-    for (uint64_t w = 1; w <= bmax && w <= n; w <<= 1) ++nlev;
+    for (uint64_t w = 1; w <= bmax && w <= (uint64_t)n; w <<= 1) ++nlev;
     const double thr = ctx.cp.threshold;
     const double p2l = ldexp(1.0, max(L, -1074)), p2nl = ldexp(1.0, min(-L, 1023));
     if (warp == 0 && (uint32_t)lane < nlev) {
@@ -1081,8 +1105,8 @@ __global__ void __launch_bounds__(BX_THREADS)
     for (int l = 0; l < 3; ++l) {
         const uint32_t w = 1u << l;
         if (w > bmax || w > n) continue;  // (levels stop at the first such w)
-        const uint64_t m = n - w + 1;
-        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+        const uint32_t m = n - (uint32_t)w + 1;
+        const uint32_t lim2 = m > i0 ? min(m - i0, T) : 0;
         const double cut = s_cut[l];
         int any = 0;
 #pragma unroll
@@ -1095,11 +1119,11 @@ __global__ void __launch_bounds__(BX_THREADS)
     }
     // levels w >= 8: a strip can hold an output above the cut only if max P over the strips
     // covering its partners [j0 + w, j0 + w + S) minus min P over its own outputs exceeds it
-    for (uint64_t w = 8; w <= bmax && w <= n && level < 32; w <<= 1, ++level) {
-        const uint64_t m = n - w + 1;
-        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+    for (uint32_t w = 8; w <= (uint32_t)bmax && w <= n && level < 32; w <<= 1, ++level) {
+        const uint32_t m = n - (uint32_t)w + 1;
+        const uint32_t lim2 = m > i0 ? min(m - i0, T) : 0;
         const double cut = s_cut[level];
-        const uint32_t q = (uint32_t)w / S;
+        const uint32_t q = w / S;
         const uint32_t a = min((uint32_t)tid + q, (uint32_t)BX_THREADS + 1);
         const uint32_t b = min((uint32_t)tid + q + 1, (uint32_t)BX_THREADS + 1);
         int any = 0;
@@ -1114,9 +1138,9 @@ __global__ void __launch_bounds__(BX_THREADS)
     const unsigned mask = s_mask;
     // threshold runs of the flagged levels on contiguous strips, as the tree kernel
     level = 0;
-    for (uint64_t w = 1; w <= bmax && w <= n; w <<= 1, ++level) {
-        const uint64_t m = n - w + 1;
-        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+    for (uint32_t w = 1; w <= (uint32_t)bmax && w <= n; w <<= 1, ++level) {
+        const uint32_t m = n - (uint32_t)w + 1;
+        const uint32_t lim2 = m > i0 ? min(m - i0, T) : 0;
         if (mask & (1u << level)) {
             const double sc = scale[level];
             const uint32_t lo = j0;
@@ -1158,8 +1182,8 @@ __global__ void __launch_bounds__(BX_THREADS)
     }
     // boxcar_max beyond the tile ladder: the top level's exact values for the level kernel
     if (lvl_out && n >= bmax) {
-        const uint64_t m = n - bmax + 1;
-        const uint32_t lim2 = m > i0 ? (uint32_t)(m - i0 < (uint64_t)T ? m - i0 : (uint64_t)T) : 0;
+        const uint32_t m = n - (uint32_t)bmax + 1;
+        const uint32_t lim2 = m > i0 ? min(m - i0, T) : 0;
         double* dst = lvl_out + base;
 #pragma unroll
         for (int k = 0; k < S; ++k) {
@@ -1372,7 +1396,7 @@ void launch_boxcar_peaks(const void* x, int kind, const uint32_t* row_len, const
         fprintf(stderr, "pgb boxcar: prefix kernel, %u of %llu tiles to the tree kernel\n", nfb,
                 (unsigned long long)nrows * tiles);
     }
-    const dim3 tgrid = tree ? grid : dim3(148 * 2);
+    const dim3 tgrid = tree ? grid : dim3(148);  // list mode: one wave, looping over the list
     const uint2* lst = tree ? nullptr : fb_list;
 #define PGB_BX(K, SS)                                                                        \
     do {                                                                                     \
