@@ -601,6 +601,30 @@ __global__ void __launch_bounds__(NW * 32, 1)
     }
 }
 
+#ifdef PGB_ABLATIONS
+// Two CTAs per SM (PGB_DD_2CTA=1): the same ring tile capped at 64 registers so 32 warps
+// share an SM (latency hiding) -- the stage width is halved to fit two rings in shared memory.
+template <int G, int VPT>
+__global__ void __launch_bounds__(DD_THREADS, 2)
+    dedisp_u8_ring_persist2_kernel(const DedispLaunch p, const uint8_t* __restrict__ rows,
+                                   int32_t* __restrict__ out, const uint32_t* __restrict__ blk_len) {
+    __shared__ uint32_t s_item;
+    const uint32_t nblocks = (p.nrows + 31) / 32;
+    const uint32_t items = nblocks * (p.ntiles - p.tile0);
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_item = atomicAdd(p.work_ctr, 1u);
+        __syncthreads();
+        const uint32_t item = s_item;
+        if (item >= items) return;
+        const uint32_t blk = item % nblocks, tile = p.tile0 + item / nblocks;
+        if (p.blk_first && tile < p.blk_first[blk]) continue;
+        if ((uint64_t)tile * DD_NT >= blk_len[blk]) continue;
+        ring_tile<G, VPT, 8, RING_NS, DD_WARPS>(p, rows, out, blk_len, blk, tile);
+    }
+}
+#endif
+
 // Tile-independent staging geometry of the u8 kernel, one warp per (trial block,
 // channel): the window of channel c for a block starts at i0 + (min_t d_t(c) & ~15)
 // (i0 is a multiple of DD_NT, so 16-byte aligned) and trial t reads it at
@@ -1278,6 +1302,29 @@ void launch_dedisp_u8_ablation(const DedispLaunch& p0, const uint8_t* rows, int3
         const char* e = pgb_ablation_env("PGB_DD_WARPS");
         return e && atoi(e) == 32;
     }();
+    static const bool two = [] {  // PGB_DD_2CTA=1: two 64-register CTAs per SM
+        const char* e = pgb_ablation_env("PGB_DD_2CTA");
+        return e && *e == '1';
+    }();
+    if (two && p.tpw == 2 && p.dd_off && p.work_ctr) {
+        int g = 8;
+        while (g > 1 && ring_smem_bytes(g, p.wmax) > 112 * 1024) g >>= 1;
+        const size_t rsm = ring_smem_bytes(g, p.wmax);
+        const int vpt = (int)((p.wmax / 16 + 32u * (DD_WARPS / g) - 1) / (32u * (DD_WARPS / g)));
+        if (rsm <= 112 * 1024 && g >= p.g / 2) {
+#define PGB_RING2C(G_, V_)                                                                         \
+    if (g == G_ && vpt <= V_) {                                                                    \
+        PGB_CUDA(cudaFuncSetAttribute(dedisp_u8_ring_persist2_kernel<G_, V_>,                      \
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rsm));     \
+        dedisp_u8_ring_persist2_kernel<G_, V_><<<2 * num_sms(), DD_THREADS, rsm, st>>>(p, rows, out, p.blk_len); \
+        dd_which("ring3-persist-2cta", G_, V_, 8);                                                 \
+        PGB_CUDA(cudaGetLastError());                                                              \
+        return;                                                                                    \
+    }
+            PGB_RING2C(4, 1) PGB_RING2C(4, 2) PGB_RING2C(4, 4) PGB_RING2C(8, 1) PGB_RING2C(8, 2)
+#undef PGB_RING2C
+        }
+    }
     if (ring && !v1 && !sf && p.tpw == 2 && p.dd_off && nw32 && p.work_ctr) {
         int g = 8;
         while (g > 1 && ring_smem_bytes(g, p.wmax) > 227 * 1024) g >>= 1;
