@@ -85,3 +85,4 @@ def test_spike_tiles_are_handed_to_the_tree_kernel():
     assert lines, out.stderr[-2000:]
     nfb, tot = int(lines[-1].split()[4]), int(lines[-1].split()[6])
     assert 0 < nfb < tot, lines
+

@@ -87,12 +87,13 @@ def test_dense_flags_take_the_float_fallback(abl_engine, ref, monkeypatch):
     assert bs.sum() > 16 * 10
 
 
+@pytest.mark.parametrize("nch", [192, 100])  # 100: partial 64-channel tiles, rows not 16-byte multiples
 @pytest.mark.parametrize("narrow,broad,local_mean", [(True, True, False), (True, False, True),
                                                      (False, True, False)])
-def test_integer_masks_take_the_u8_path(engine, ref, narrow, broad, local_mean):
+def test_integer_masks_take_the_u8_path(engine, ref, narrow, broad, local_mean, nch):
     """Zero replacement or bad channels only: every cell stays an integer, the transpose zeroes
     the masked cells and the integer kernel runs."""
-    hdr, plan, data = _case(16000, 192, 250.0, 2.0, 500, seed=5)
+    hdr, plan, data = _case(16000, nch, 250.0, 2.0, 500, seed=5)
     _check(engine, ref, hdr, plan, data, RfiConfig(narrowband=narrow, broadband=broad, local_mean=local_mean))
 
 
