@@ -240,6 +240,10 @@ pgb_status pgb_stream_begin(pgb_context* ctx, uint64_t nsamples, const pgb_chunk
 pgb_status pgb_stream_buffer(pgb_context* ctx, size_t chunk, uint8_t** host_buffer,
                              size_t* capacity);
 pgb_status pgb_stream_push(pgb_context* ctx, size_t chunk, const uint8_t* bytes);
+/* Optional: start chunk k's upload from its pinned buffer as soon as it is filled (a
+ * reader thread may call it for chunk k+1 while chunk k is being pushed), so the copy
+ * overlaps chunk k's compute instead of starting inside pgb_stream_push(k+1). */
+pgb_status pgb_stream_upload(pgb_context* ctx, size_t chunk);
 pgb_status pgb_stream_finish(pgb_context* ctx, size_t* n_candidates, size_t* n_clusters);
 
 /* ---- multi-GPU payload fan-out ------------------------------------------------ */

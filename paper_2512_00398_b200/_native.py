@@ -66,6 +66,7 @@ SIGNATURES = {
                           _P(abi.RfiConfigC)], _int),
     "pgb_stream_buffer": ([_vp, _sz, _P(_vp), _P(_sz)], _int),
     "pgb_stream_push": ([_vp, _sz, _vp], _int),
+    "pgb_stream_upload": ([_vp, _sz], _int),
     "pgb_stream_finish": ([_vp, _P(_sz), _P(_sz)], _int),
     "pgb_device_alloc": ([_int, _sz, _P(_vp)], _int),
     "pgb_device_free": ([_int, _vp], _int),

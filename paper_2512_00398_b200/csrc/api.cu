@@ -218,6 +218,8 @@ struct pgb_context {
         DevBuf dbuf[2];
         cudaEvent_t up_done[2] = {}, dev_free[2] = {};
         bool up_pending[2] = {false, false}, dev_pending[2] = {false, false};
+        int64_t uploaded[2] = {-1, -1};  // chunk whose upload was issued into buffer b (not yet pushed)
+        std::mutex mu;                   // pgb_stream_upload (reader thread) vs pgb_stream_push
     } stream;
     // host repack of widened 8-bit float chunks (pgb_run_dm_loop_f32 with host data)
     PinnedBuf h_pack;
@@ -1857,6 +1859,7 @@ pgb_status pgb_stream_begin(pgb_context* ctx, uint64_t nsamples, const pgb_chunk
         S.has_rfi = rfi && (rfi->narrowband || rfi->broadband);
         if (S.has_rfi) S.rfi = *rfi;
         S.next = 0;
+        S.uploaded[0] = S.uploaded[1] = -1;
         S.total = 0;
         S.pending = false;
         S.overlap = cfg->baseline_window > 0;
@@ -1898,6 +1901,38 @@ pgb_status pgb_stream_buffer(pgb_context* ctx, size_t k, uint8_t** host_buffer, 
     });
 }
 
+namespace {
+// H2D of chunk k into device buffer k & 1 on the copy stream (caller holds S.mu)
+void stream_upload(pgb_context* ctx, size_t k, const uint8_t* bytes) {
+    auto& S = ctx->stream;
+    const int b = (int)(k & 1);
+    const size_t cb = (size_t)S.chunks[k].length * ctx->nchans;
+    // the device buffer held chunk k-2 until its front half (transpose / RFI) read it
+    if (S.dev_pending[b]) PGB_CUDA(cudaStreamWaitEvent(ctx->copy_st, S.dev_free[b], 0));
+    if (bytes && bytes != S.hbuf[b].as<uint8_t>() && S.up_pending[b]) {
+        PGB_CUDA(cudaEventSynchronize(S.up_done[b]));
+        S.up_pending[b] = false;
+    }
+    PGB_CUDA(cudaMemcpyAsync(S.dbuf[b].p, bytes ? bytes : S.hbuf[b].as<uint8_t>(), cb,
+                             cudaMemcpyHostToDevice, ctx->copy_st));
+    PGB_CUDA(cudaEventRecord(S.up_done[b], ctx->copy_st));
+    S.up_pending[b] = true;
+    S.uploaded[b] = (int64_t)k;
+}
+}  // namespace
+
+pgb_status pgb_stream_upload(pgb_context* ctx, size_t k) {
+    return guarded([&] {
+        need(ctx, PGB_ERR_ARGUMENT, "null ctx");
+        auto& S = ctx->stream;
+        std::lock_guard<std::mutex> lock(S.mu);
+        need(S.open && k >= S.next && k <= S.next + 1 && k < S.chunks.size(), PGB_ERR_ARGUMENT,
+             "stream upload requested out of order (next or next + 1 only)");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        if (S.uploaded[k & 1] != (int64_t)k) stream_upload(ctx, k, nullptr);
+    });
+}
+
 pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
     return guarded([&] {
         NvtxRange nvtx("pgb stream push");
@@ -1909,20 +1944,16 @@ pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
         // staging arena of the small per-chunk uploads is free again
         if (k > 0) stage_reset(ctx);
         const pgb_chunk_spec& spec = S.chunks[k];
-        const uint32_t C = ctx->nchans;
         const int b = (int)(k & 1);
-        const size_t cb = (size_t)spec.length * C;
-        // the device buffer held chunk k-2 until its front half (transpose / RFI) read it
-        if (S.dev_pending[b]) PGB_CUDA(cudaStreamWaitEvent(ctx->copy_st, S.dev_free[b], 0));
-        if (bytes && bytes != S.hbuf[b].as<uint8_t>() && S.up_pending[b]) {
-            PGB_CUDA(cudaEventSynchronize(S.up_done[b]));
-            S.up_pending[b] = false;
+        {
+            std::lock_guard<std::mutex> lock(S.mu);
+            // already uploaded by pgb_stream_upload (from the caller's own buffer only if
+            // that is where the bytes are)
+            if (S.uploaded[b] != (int64_t)k || (bytes && bytes != S.hbuf[b].as<uint8_t>()))
+                stream_upload(ctx, k, bytes);
+            S.uploaded[b] = -1;
+            PGB_CUDA(cudaStreamWaitEvent(ctx->st, S.up_done[b], 0));
         }
-        PGB_CUDA(cudaMemcpyAsync(S.dbuf[b].p, bytes ? bytes : S.hbuf[b].as<uint8_t>(), cb,
-                                 cudaMemcpyHostToDevice, ctx->copy_st));
-        PGB_CUDA(cudaEventRecord(S.up_done[b], ctx->copy_st));
-        S.up_pending[b] = true;
-        PGB_CUDA(cudaStreamWaitEvent(ctx->st, S.up_done[b], 0));
         trace_mark(ctx, "chunk upload waited", ctx->st);
         const uint8_t* cptr = S.dbuf[b].as<uint8_t>();
         ChunkInput ci{cptr, true};
@@ -1937,8 +1968,11 @@ pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
         ChunkRun* runs = S.runs->r;
         ChunkRun& cur = runs[k & 1];
         chunk_front(ctx, ci, &spec, &S.cfg, (int)(k & 1), cur);
-        PGB_CUDA(cudaEventRecord(S.dev_free[b], ctx->st));
-        S.dev_pending[b] = true;
+        {
+            std::lock_guard<std::mutex> lock(S.mu);
+            PGB_CUDA(cudaEventRecord(S.dev_free[b], ctx->st));
+            S.dev_pending[b] = true;
+        }
         if (S.pending) append_chunk_sync(ctx, runs[(k - 1) & 1], S.total);
         S.pending = true;
         if (!S.overlap) {

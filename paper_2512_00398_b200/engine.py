@@ -401,7 +401,7 @@ class Engine:
 
     def search_stream(self, fd: int, data_offset: int, nsamples: int, chunks: list[ChunkSpec],
                       plan: DmTrialPlan, cfg: EngineConfig, *, trial_range: tuple[int, int] | None = None,
-                      cluster: bool = True, rfi: RfiConfig | None = None, read_threads: int = 4):
+                      cluster: bool = True, rfi: RfiConfig | None = None, read_threads: int = 8):
         """execute_task with the prefetching reader on an open 8-bit filterbank (bounded memory).
 
         Chunk k is read from `fd` (payload at `data_offset`, [nsamples][nchans] bytes) by
@@ -442,6 +442,8 @@ class Engine:
                     a += n
 
             list(pool.map(rd, range(0, nbytes, step)))
+            # start the upload now: it overlaps the previous chunk's compute
+            self._check(self._lib.pgb_stream_upload(self._h, k))
 
         import time
 

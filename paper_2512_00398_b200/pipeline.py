@@ -224,7 +224,7 @@ def create_file_task(path: str, params: SearchParams, output_path: str, index: i
     return PipelineTask(index, str(path), output_path, create_task(hdr, params), off)
 
 
-def execute_task(pt: PipelineTask, eng, read_threads: int = 4) -> FileOutcome:
+def execute_task(pt: PipelineTask, eng, read_threads: int = 8) -> FileOutcome:
     """execute_task (src/pipeline.cpp:61-119) on the device: streamed chunks (bounded memory),
     the chunk chain, file sort + link_grid, one .cand file; stage times in the outcome."""
     import os
@@ -255,7 +255,7 @@ def execute_task(pt: PipelineTask, eng, read_threads: int = 4) -> FileOutcome:
 
 def run_multi_file(paths: list[str], params: SearchParams, output_dir: str, n_create: int = 1,
                    n_exec: int = 2, creation_capacity: int = 0, execution_capacity: int = 0, *,
-                   devices: tuple[int, ...] = (0,), read_threads: int = 4) -> RunSummary:
+                   devices: tuple[int, ...] = (0,), read_threads: int = 8) -> RunSummary:
     """Two-stage multi-file pipeline (src/pipeline.cpp:136-210): n_create workers parse
     headers and build plans, n_exec workers execute them through bounded queues (capacity
     2x the stage's workers by default), per-file failures isolated into the summary.  Each
@@ -416,7 +416,7 @@ def read_filterbank(path: str | Path) -> tuple[FilterbankHeader, np.ndarray]:
     return hdr, payload.reshape(-1, hdr.nchans)
 
 
-def search_fil(path: str | Path, params: SearchParams, *, device: int = 0, read_threads: int = 4,
+def search_fil(path: str | Path, params: SearchParams, *, device: int = 0, read_threads: int = 8,
                trial_range: tuple[int, int] | None = None) -> SearchResult:
     """create_task + execute_task on an 8-bit SIGPROC file with bounded memory
     (src/pipeline.cpp:32-119): chunks are read straight into pinned buffers by parallel
