@@ -46,6 +46,7 @@ typedef enum pgb_status {
     PGB_ERR_INVALID_PLAN = 6,    /* pulsegrid::invalid_plan_error      errors.hpp:24-26 */
     PGB_ERR_ARGUMENT = 7,        /* bad pointer / size (std::invalid_argument) */
     PGB_ERR_INSUFFICIENT = 8,    /* pulsegrid::insufficient_statistics_error errors.hpp:40-42 */
+    PGB_ERR_READ = 9,            /* pulsegrid::read_error              errors.hpp:29-34 */
     PGB_ERR_NO_DEVICE = 100,     /* no sm_100 device visible */
     PGB_ERR_CUDA = 101,          /* CUDA runtime / kernel failure */
     PGB_ERR_OOM = 102            /* device allocation failed */
@@ -244,6 +245,15 @@ pgb_status pgb_stream_push(pgb_context* ctx, size_t chunk, const uint8_t* bytes)
  * reader thread may call it for chunk k+1 while chunk k is being pushed), so the copy
  * overlaps chunk k's compute instead of starting inside pgb_stream_push(k+1). */
 pgb_status pgb_stream_upload(pgb_context* ctx, size_t chunk);
+/* Optional, progressive: upload piece `part` of `nparts` (rows [r(part), r(part+1)) of
+ * chunk k, r(j) = floor(floor(L*j/nparts)/64)*64 and r(nparts) = L, L the chunk length)
+ * as soon as that piece of the stream buffer
+ * is filled, from any thread and in any order (ok = 0: the piece could not be read).
+ * Announce the pieces first (part = 0, ok = -1: nothing uploaded) before the push can
+ * happen.  pgb_stream_push(k) then transposes and dedisperses the chunk's tiles piece by piece as
+ * their rows arrive, so the first chunk's read overlaps its own compute; it fails with
+ * PGB_ERR_READ if a piece was reported unread. */
+pgb_status pgb_stream_upload_part(pgb_context* ctx, size_t chunk, size_t part, size_t nparts, int ok);
 pgb_status pgb_stream_finish(pgb_context* ctx, size_t* n_candidates, size_t* n_clusters);
 
 /* ---- multi-GPU payload fan-out ------------------------------------------------ */

@@ -67,6 +67,7 @@ SIGNATURES = {
     "pgb_stream_buffer": ([_vp, _sz, _P(_vp), _P(_sz)], _int),
     "pgb_stream_push": ([_vp, _sz, _vp], _int),
     "pgb_stream_upload": ([_vp, _sz], _int),
+    "pgb_stream_upload_part": ([_vp, _sz, _sz, _sz, _int], _int),
     "pgb_stream_finish": ([_vp, _P(_sz), _P(_sz)], _int),
     "pgb_device_alloc": ([_int, _sz, _P(_vp)], _int),
     "pgb_device_free": ([_int, _vp], _int),

@@ -18,6 +18,7 @@
 
 #include <chrono>
 #include <cstdio>
+#include <condition_variable>
 #include <functional>
 
 #include "pgb_internal.h"
@@ -220,6 +221,12 @@ struct pgb_context {
         bool up_pending[2] = {false, false}, dev_pending[2] = {false, false};
         int64_t uploaded[2] = {-1, -1};  // chunk whose upload was issued into buffer b (not yet pushed)
         std::mutex mu;                   // pgb_stream_upload (reader thread) vs pgb_stream_push
+        // progressive pieces of one chunk (pgb_stream_upload_part): the chunk, piece ends
+        // and events, which pieces have been issued / failed
+        int64_t part_chunk = -1;
+        std::vector<std::pair<uint64_t, cudaEvent_t>> parts;
+        std::vector<char> part_state;  // 0 pending, 1 issued, 2 failed
+        std::condition_variable cv;
     } stream;
     // host repack of widened 8-bit float chunks (pgb_run_dm_loop_f32 with host data)
     PinnedBuf h_pack;
@@ -267,6 +274,10 @@ struct ChunkInput {
     const uint8_t* samp_bad = nullptr;
     bool h16 = false;
     std::function<ChunkInput()> fallback;
+    // progressive chunk whose pieces are uploaded by another thread (streaming search):
+    // called with the piece index before its event is waited on; returns once the piece's
+    // upload has been issued (or throws)
+    std::function<void(size_t)> seg_ready;
 };
 
 // Validation and in-flight arithmetic of run_dm_loop (src/engine.cpp:60-97).
@@ -550,8 +561,16 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     // 1. transpose to channel-major rows (a progressive chunk transposes per sub-segment
     // below, interleaved with the dedispersion of the tiles it completes)
     const bool progressive = u8 && in.prog && !ws_g && !in.prog->empty() && wide_rows.empty();
-    if (in.prog && !in.prog->empty() && !progressive)  // whole chunk first
-        PGB_CUDA(cudaStreamWaitEvent(st, in.prog->back().second, 0));
+    if (in.prog && !in.prog->empty() && !progressive) {  // whole chunk first
+        if (in.seg_ready) {  // pieces uploaded in any order by another thread: wait for each
+            for (size_t j = 0; j < in.prog->size(); ++j) {
+                in.seg_ready(j);
+                PGB_CUDA(cudaStreamWaitEvent(st, (*in.prog)[j].second, 0));
+            }
+        } else {
+            PGB_CUDA(cudaStreamWaitEvent(st, in.prog->back().second, 0));
+        }
+    }
     if (u8) {
         if (in.chan_bad)  // RFI zero mask: integer cells, bad channels and rows zeroed
             launch_transpose_masked(static_cast<const uint8_t*>(in.data), L, C, in.chan_bad, in.samp_bad,
@@ -665,8 +684,11 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
             // start rounded down to 16, whole 16-byte vectors, one extra word)
             uint64_t a = 0;
             uint32_t done = 0;
+            size_t segi = 0;
             for (const auto& seg : *in.prog) {
                 const uint64_t b = std::min<uint64_t>(seg.first, L);
+                if (in.seg_ready) in.seg_ready(segi);
+                ++segi;
                 PGB_CUDA(cudaStreamWaitEvent(st, seg.second, 0));
                 if (b > a) {
                     launch_transpose_u8(static_cast<const uint8_t*>(in.data) + a * C, b - a, C,
@@ -1208,10 +1230,33 @@ pgb_status pgb_generate_dm_trials(double dm_lo, double dm_hi, const pgb_header* 
         if (!dms) return;
         need(capacity >= out.size(), PGB_ERR_ARGUMENT, "capacity too small");
         std::copy(out.begin(), out.end(), dms);
-        if (delays)
-            for (size_t t = 0; t < out.size(); ++t)
-                for (uint32_t c = 0; c < h->nchans; ++c)
-                    delays[t * h->nchans + c] = delay_samples(out[t], h, c);
+        if (delays) {
+            // delay_samples evaluates (k * dm) * (1/f_c^2 - 1/f_ref^2) left to right: the
+            // channel factor is the same double for every trial, so it is formed once per
+            // channel (same operations, same bits); trials are split over host threads
+            const uint32_t C = h->nchans;
+            const double f_ref = max_freq(h);
+            std::vector<double> fac(C);
+            for (uint32_t c = 0; c < C; ++c) {
+                const double f_c = channel_freq(h, c);
+                fac[c] = 1.0 / (f_c * f_c) - 1.0 / (f_ref * f_ref);
+            }
+            const size_t T = out.size();
+            auto rows = [&](size_t t0, size_t t1) {
+                for (size_t t = t0; t < t1; ++t) {
+                    const double kd = k_dispersion * out[t];
+                    int64_t* d = delays + t * C;
+                    for (uint32_t c = 0; c < C; ++c) d[c] = (int64_t)std::floor(kd * fac[c] / h->tsamp + 0.5);
+                }
+            };
+            const size_t nth = (size_t)T * C >= (1u << 20)
+                                   ? std::min<size_t>(T, std::max(1u, std::min(16u, std::thread::hardware_concurrency())))
+                                   : 1;
+            std::vector<std::thread> pool;
+            for (size_t i = 1; i < nth; ++i) pool.emplace_back(rows, T * i / nth, T * (i + 1) / nth);
+            rows(0, T / nth);
+            for (auto& th : pool) th.join();
+        }
     });
 }
 
@@ -1860,6 +1905,7 @@ pgb_status pgb_stream_begin(pgb_context* ctx, uint64_t nsamples, const pgb_chunk
         if (S.has_rfi) S.rfi = *rfi;
         S.next = 0;
         S.uploaded[0] = S.uploaded[1] = -1;
+        S.part_chunk = -1;
         S.total = 0;
         S.pending = false;
         S.overlap = cfg->baseline_window > 0;
@@ -1902,6 +1948,12 @@ pgb_status pgb_stream_buffer(pgb_context* ctx, size_t k, uint8_t** host_buffer, 
 }
 
 namespace {
+// first row of piece j of nparts (multiples of 64 rows: the progressive transpose writes
+// 16-byte vectors at the piece start; the last piece ends at L)
+uint64_t stream_piece_row(uint64_t L, size_t j, size_t nparts) {
+    return j >= nparts ? L : L * j / nparts / 64 * 64;
+}
+
 // H2D of chunk k into device buffer k & 1 on the copy stream (caller holds S.mu)
 void stream_upload(pgb_context* ctx, size_t k, const uint8_t* bytes) {
     auto& S = ctx->stream;
@@ -1933,6 +1985,49 @@ pgb_status pgb_stream_upload(pgb_context* ctx, size_t k) {
     });
 }
 
+pgb_status pgb_stream_upload_part(pgb_context* ctx, size_t k, size_t part, size_t nparts, int ok) {
+    return guarded([&] {
+        need(ctx && nparts > 0 && part < nparts, PGB_ERR_ARGUMENT, "bad piece");
+        auto& S = ctx->stream;
+        std::unique_lock<std::mutex> lock(S.mu);
+        need(S.open && k >= S.next && k <= S.next + 1 && k < S.chunks.size(), PGB_ERR_ARGUMENT,
+             "stream piece requested out of order (next or next + 1 only)");
+        PGB_CUDA(cudaSetDevice(ctx->device));
+        if (S.part_chunk != (int64_t)k) {
+            need(S.part_chunk < 0 || (int64_t)k > S.part_chunk, PGB_ERR_ARGUMENT, "pieces of two chunks at once");
+            S.part_chunk = (int64_t)k;
+            const uint64_t L = S.chunks[k].length;
+            while (S.parts.size() < nparts) {
+                cudaEvent_t e;
+                PGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                S.parts.emplace_back(0, e);
+            }
+            for (size_t j = 0; j < S.parts.size(); ++j) S.parts[j].first = j < nparts ? stream_piece_row(L, j + 1, nparts) : 0;
+            S.part_state.assign(nparts, 0);
+            const int b = (int)(k & 1);
+            // the device buffer held chunk k-2 until its front half read it
+            if (S.dev_pending[b]) PGB_CUDA(cudaStreamWaitEvent(ctx->copy_st, S.dev_free[b], 0));
+        }
+        need(S.part_state.size() == nparts, PGB_ERR_ARGUMENT, "piece count changed within a chunk");
+        if (ok < 0) {
+            // announcement only: pgb_stream_push(k) will wait for the pieces
+        } else if (!ok) {
+            S.part_state[part] = 2;
+        } else if (S.part_state[part] == 0) {
+            const int b = (int)(k & 1);
+            const size_t C = ctx->nchans;
+            const uint64_t L = S.chunks[k].length;
+            const uint64_t r0 = stream_piece_row(L, part, nparts), r1 = stream_piece_row(L, part + 1, nparts);
+            if (r1 > r0)
+                PGB_CUDA(cudaMemcpyAsync(S.dbuf[b].as<uint8_t>() + r0 * C, S.hbuf[b].as<uint8_t>() + r0 * C,
+                                         (r1 - r0) * C, cudaMemcpyHostToDevice, ctx->copy_st));
+            PGB_CUDA(cudaEventRecord(S.parts[part].second, ctx->copy_st));
+            S.part_state[part] = 1;
+        }
+        S.cv.notify_all();
+    });
+}
+
 pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
     return guarded([&] {
         NvtxRange nvtx("pgb stream push");
@@ -1945,14 +2040,22 @@ pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
         if (k > 0) stage_reset(ctx);
         const pgb_chunk_spec& spec = S.chunks[k];
         const int b = (int)(k & 1);
+        const bool pieces = S.part_chunk == (int64_t)k;  // uploaded piece by piece (progressive)
+        std::vector<std::pair<uint64_t, cudaEvent_t>> prog;
         {
             std::lock_guard<std::mutex> lock(S.mu);
-            // already uploaded by pgb_stream_upload (from the caller's own buffer only if
-            // that is where the bytes are)
-            if (S.uploaded[b] != (int64_t)k || (bytes && bytes != S.hbuf[b].as<uint8_t>()))
-                stream_upload(ctx, k, bytes);
-            S.uploaded[b] = -1;
-            PGB_CUDA(cudaStreamWaitEvent(ctx->st, S.up_done[b], 0));
+            if (pieces) {
+                need(!bytes || bytes == S.hbuf[b].as<uint8_t>(), PGB_ERR_ARGUMENT,
+                     "a chunk uploaded in pieces is pushed from its stream buffer");
+                prog.assign(S.parts.begin(), S.parts.begin() + (long)S.part_state.size());
+            } else {
+                // already uploaded by pgb_stream_upload (from the caller's own buffer only if
+                // that is where the bytes are)
+                if (S.uploaded[b] != (int64_t)k || (bytes && bytes != S.hbuf[b].as<uint8_t>()))
+                    stream_upload(ctx, k, bytes);
+                S.uploaded[b] = -1;
+                PGB_CUDA(cudaStreamWaitEvent(ctx->st, S.up_done[b], 0));
+            }
         }
         trace_mark(ctx, "chunk upload waited", ctx->st);
         const uint8_t* cptr = S.dbuf[b].as<uint8_t>();
@@ -1960,6 +2063,22 @@ pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
         ci.raw = true;
         ci.pitch_min = S.pitch_min;
         ci.more = S.overlap && k + 1 < S.chunks.size();
+        auto wait_piece = [&S](size_t j) {
+            std::unique_lock<std::mutex> lock(S.mu);
+            S.cv.wait(lock, [&] { return S.part_state[j] != 0; });
+            if (S.part_state[j] == 2) raise(PGB_ERR_READ, "stream piece " + std::to_string(j) + " was not read");
+        };
+        if (pieces) {
+            if (k == 0 && !S.has_rfi) {  // progressive transpose + dedispersion (chunk_front)
+                ci.prog = &prog;
+                ci.seg_ready = wait_piece;
+            } else {  // RFI excision and overlap reuse need the whole chunk first
+                for (size_t j = 0; j < prog.size(); ++j) {
+                    wait_piece(j);
+                    PGB_CUDA(cudaStreamWaitEvent(ctx->st, prog[j].second, 0));
+                }
+            }
+        }
         if (S.has_rfi) {  // src/pipeline.cpp:79-87
             ci = rfi_input(ctx, cptr, spec.length, &S.rfi);
             ci.pitch_min = S.pitch_min;
@@ -1972,6 +2091,12 @@ pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
             std::lock_guard<std::mutex> lock(S.mu);
             PGB_CUDA(cudaEventRecord(S.dev_free[b], ctx->st));
             S.dev_pending[b] = true;
+            if (pieces) {  // every piece was issued (chunk_front waited for each): the host
+                // buffer is free once the copy stream is past them
+                PGB_CUDA(cudaEventRecord(S.up_done[b], ctx->copy_st));
+                S.up_pending[b] = true;
+                S.part_chunk = -1;
+            }
         }
         if (S.pending) append_chunk_sync(ctx, runs[(k - 1) & 1], S.total);
         S.pending = true;

@@ -445,20 +445,59 @@ class Engine:
             # start the upload now: it overlaps the previous chunk's compute
             self._check(self._lib.pgb_stream_upload(self._h, k))
 
+        def piece(j: int, npieces: int, mv, off0: int, nbytes: int) -> None:
+            """Piece j of chunk 0 (its rows as the library splits them), uploaded when read."""
+            L = chunks[0].length
+
+            def row(i: int) -> int:  # the library's piece boundaries (pgb_stream_upload_part)
+                return L if i >= npieces else L * i // npieces // 64 * 64
+
+            a, b = row(j) * C, row(j + 1) * C
+            ok = 0
+            try:
+                while a < b:
+                    n = os.preadv(fd, [mv[a:b]], off0 + a)
+                    if n <= 0:
+                        raise OSError(f"short read at byte {off0 + a}")
+                    a += n
+                ok = 1
+            finally:
+                self._check(self._lib.pgb_stream_upload_part(self._h, 0, j, npieces, ok))
+
         import time
 
         t_read = 0.0
         t0 = time.perf_counter()
+        # chunk 0 is read and uploaded piece by piece and its tiles computed as the rows
+        # arrive (RFI excision needs whole chunks)
+        progressive = bool(chunks) and rc is None
         try:
             with ThreadPoolExecutor(1) as reader:
-                fut = reader.submit(fill, 0) if chunks else None
+                pieces = []
+                if progressive:
+                    p, cap = ctypes.c_void_p(), ctypes.c_size_t()
+                    self._check(self._lib.pgb_stream_buffer(self._h, 0, ctypes.byref(p), ctypes.byref(cap)))
+                    nb0 = chunks[0].length * C
+                    mv0 = memoryview((ctypes.c_uint8 * nb0).from_address(p.value)).cast("B")
+                    npieces = max(2, read_threads)
+                    off0 = data_offset + chunks[0].start_sample * C
+                    # announce the pieces, so the push below waits for them
+                    self._check(self._lib.pgb_stream_upload_part(self._h, 0, 0, npieces, -1))
+                    pieces = [pool.submit(piece, j, npieces, mv0, off0, nb0) for j in range(npieces)]
+                    fut = reader.submit(fill, 1) if len(chunks) > 1 else None
+                else:
+                    fut = reader.submit(fill, 0) if chunks else None
                 for k in range(len(chunks)):
-                    tw = time.perf_counter()
-                    fut.result()  # waiting here = the reader is behind the device
-                    t_read += time.perf_counter() - tw
-                    if k + 1 < len(chunks):
-                        fut = reader.submit(fill, k + 1)
+                    if not (progressive and k == 0):
+                        tw = time.perf_counter()
+                        fut.result()  # waiting here = the reader is behind the device
+                        t_read += time.perf_counter() - tw
+                        if k + 1 < len(chunks):
+                            fut = reader.submit(fill, k + 1)
                     self._check(self._lib.pgb_stream_push(self._h, k, None))
+                    if progressive and k == 0:
+                        for f in pieces:
+                            f.result()
         finally:
             pool.shutdown()
         nc, ncl = ctypes.c_size_t(), ctypes.c_size_t()

@@ -43,6 +43,10 @@ class InsufficientStatisticsError(PulsegridError):
     """pulsegrid::insufficient_statistics_error (errors.hpp:40-42)."""
 
 
+class ReadError(PulsegridError):
+    """pulsegrid::read_error (errors.hpp:29-34): a chunk of the file could not be read."""
+
+
 class DeviceError(PulsegridError):
     """No usable sm_100 device, a CUDA failure, or device OOM (no CPU fallback exists)."""
 
@@ -56,6 +60,7 @@ _BY_CODE = {
     6: InvalidPlanError,
     7: ValueError,
     8: InsufficientStatisticsError,
+    9: ReadError,
     100: DeviceError,
     101: DeviceError,
     102: DeviceError,
