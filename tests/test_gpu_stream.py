@@ -93,6 +93,56 @@ def test_search_fil_many_chunks_equals_payload_search(tmp_path, engine, rfi):
     _assert_same(res, cands, clusters, skipped)
 
 
+@pytest.mark.parametrize("read_threads", [1, 3, 16])
+def test_first_chunk_pieces_any_count(tmp_path, engine, read_threads):
+    """The first chunk is read and uploaded in max(2, read_threads) 64-row-aligned pieces and
+    computed as they arrive: any piece count gives the whole-payload search's result."""
+    from paper_2512_00398_b200.pipeline import search_fil
+    from tools import synth
+
+    cfg = dict(synth.CONFIGS["A"], nsamples=50000, nsamps_chunk=30000, boxcar_max=256, npulses=4,
+               seed=78, dm_hi=150.0)
+    task = task_for(cfg)
+    path = tmp_path / "pieces.fil"
+    synth.write_filterbank(path, cfg, task.plan.delays)
+    res = search_fil(path, _params(cfg), read_threads=read_threads)
+    payload = synth.payload(cfg, task.plan.delays)
+    cands, clusters, skipped = engine.search_file(payload, cfg["nsamples"], task.chunks, task.plan,
+                                                  task.engine)
+    assert len(cands) > 0
+    _assert_same(res, cands, clusters, skipped)
+
+
+def test_unreadable_piece_fails_the_push(tmp_path, monkeypatch):
+    """A piece of the first chunk that cannot be read is reported to the library
+    (pgb_stream_upload_part with ok = 0): the push fails with pulsegrid::read_error instead of
+    searching stale bytes, and the engine streams the next file normally."""
+    import os
+
+    from paper_2512_00398_b200.errors import ReadError
+    from paper_2512_00398_b200.pipeline import search_fil
+    from tools import synth
+
+    cfg = dict(synth.CONFIGS["A"], nsamples=50000, nsamps_chunk=30000, boxcar_max=256, seed=79, dm_hi=150.0)
+    task = task_for(cfg)
+    path = tmp_path / "bad.fil"
+    synth.write_filterbank(path, cfg, task.plan.delays)
+    real = os.preadv
+    bad_at = 15000 * cfg["nchans"]  # inside the first chunk
+
+    def flaky(fd, bufs, off):
+        if off <= bad_at < off + sum(len(b) for b in bufs):
+            raise OSError("simulated read failure")
+        return real(fd, bufs, off)
+
+    monkeypatch.setattr(os, "preadv", flaky)
+    with pytest.raises(ReadError):
+        search_fil(path, _params(cfg), read_threads=4)
+    monkeypatch.setattr(os, "preadv", real)
+    res = search_fil(path, _params(cfg), read_threads=4)
+    assert len(res.candidates) > 0
+
+
 @pytest.mark.slow
 def test_search_fil_host_memory_is_bounded(tmp_path):
     """Peak RSS of a process streaming the 4 GiB config-B file stays far below the file size
