@@ -1933,6 +1933,7 @@ pgb_status pgb_stream_buffer(pgb_context* ctx, size_t k, uint8_t** host_buffer, 
     return guarded([&] {
         need(ctx && host_buffer, PGB_ERR_ARGUMENT, "null argument");
         auto& S = ctx->stream;
+        std::lock_guard<std::mutex> lock(S.mu);  // the reader thread calls this during a push
         // the next chunk's buffer, or the one after it (a reader thread fills chunk k+1
         // while chunk k is being pushed)
         need(S.open && k >= S.next && k <= S.next + 1 && k < S.chunks.size(), PGB_ERR_ARGUMENT,
@@ -2104,7 +2105,10 @@ pgb_status pgb_stream_push(pgb_context* ctx, size_t k, const uint8_t* bytes) {
             append_chunk_sync(ctx, cur, S.total);
             S.pending = false;
         }
-        ++S.next;
+        {
+            std::lock_guard<std::mutex> lock(S.mu);
+            ++S.next;
+        }
     });
 }
 
