@@ -1002,7 +1002,8 @@ __global__ void __launch_bounds__(BX_THREADS)
 #pragma unroll
     for (int k = 0; k < S; ++k) {
         const float f = j0 + k < nin ? __fdiv_rn(xs[XP(j0 + k)], frms) : 0.0f;
-        const float af = fabsf(f);
+        const float af = fabsf(f);  // (no -0 reaches here: series sums start at +0.0f, the
+        // baseline's exact zeros are +0, so all-(-0) tree ranges cannot occur)
         fhi = fmaxf(fhi, af);
         flo = fminf(flo, af > 0.0f ? af : INFINITY);
         ps[k + 1] = __dadd_rn(ps[k], (double)f);
