@@ -183,15 +183,26 @@ __device__ __forceinline__ void baseline_interior(const int32_t* __restrict__ x,
                                                   int64_t s0, int64_t s1, uint32_t hh, long long carry,
                                                   double inv_full, int lane) {
     constexpr int RB = (3 - R) & 3;  // (-1 - h) mod 4
-    for (uint32_t base = (uint32_t)s0; base < (uint32_t)s1; base += 128) {
+    // the next 128 samples' loads are issued before this block's scan (the carry chain
+    // serialises the blocks, the loads do not depend on it)
+    auto fetch = [&](uint32_t base, int4& xq, int4& a0, int4& a1, int4& b0, int4& b1) {
         const uint32_t i4 = base + 4 * lane;
-        const int4 xq = *reinterpret_cast<const int4*>(x + i4);  // 16-byte aligned (pitch, base)
+        xq = *reinterpret_cast<const int4*>(x + i4);  // 16-byte aligned (pitch, base)
         const int4* pa = reinterpret_cast<const int4*>(x + i4 + hh - R);
         const int4* pb = reinterpret_cast<const int4*>(x + i4 - 1 - hh - RB);
-        const int4 a0 = pa[0], a1 = pa[1], b0 = pb[0], b1 = pb[1];
+        a0 = pa[0];
+        a1 = pa[1];
+        b0 = pb[0];
+        b1 = pb[1];
+    };
+    int4 xq, a0, a1, b0, b1;
+    fetch((uint32_t)s0, xq, a0, a1, b0, b1);
+    for (uint32_t base = (uint32_t)s0; base < (uint32_t)s1; base += 128) {
         const int32_t av[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
         const int32_t bv[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
         const int32_t xv[4] = {xq.x, xq.y, xq.z, xq.w};
+        if (base + 128 < (uint32_t)s1) fetch(base + 128, xq, a0, a1, b0, b1);
+        const uint32_t i4 = base + 4 * lane;
         int32_t d[4];
         int32_t local = 0;
 #pragma unroll
@@ -216,7 +227,7 @@ __device__ __forceinline__ void baseline_interior(const int32_t* __restrict__ x,
     }
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)  // 32 warps per SM: latency-bound on its loads
     baseline_warp_kernel(const int32_t* __restrict__ x_all, float* __restrict__ out_all,
                          const uint32_t* __restrict__ row_len, uint64_t pitch, uint64_t window,
                          uint32_t nrows, uint32_t nseg, uint32_t nb, const long long* __restrict__ bsum) {
