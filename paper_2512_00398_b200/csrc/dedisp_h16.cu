@@ -42,10 +42,13 @@ struct HExc {
     float val;
 };
 
+// exception counts [NS][G] u32, padded to 16 bytes: the 8-byte lists and mbarriers follow
+constexpr int hx_count_words(int g) { return (H_NS * g + 3) & ~3; }
+
 size_t h16_smem_bytes(int g, uint32_t wmax) {
     return (size_t)H_NS * g * 4 * wmax                 // [NS][G][2 copies][wmax halves]
            + (size_t)H_NS * g * H_TB * 4               // offsets
-           + (size_t)H_NS * g * 4                      // exception counts
+           + (size_t)hx_count_words(g) * 4             // exception counts
            + (size_t)H_NS * g * HX_CAP * sizeof(HExc)  // exception lists
            + 2 * H_NS * sizeof(uint64_t);
 }
@@ -187,7 +190,7 @@ __device__ __forceinline__ void h16_tile(const DedispLaunch& p, const uint16_t* 
     uint8_t* buf = smem;                                                            // [NS][G][CH]
     uint32_t* offs = reinterpret_cast<uint32_t*>(smem + (size_t)NS * G * CH);      // [NS][G][TB]
     uint32_t* xcnt = offs + NS * G * TB;                                            // [NS][G]
-    HExc* xl = reinterpret_cast<HExc*>(xcnt + NS * G);                              // [NS][G][HX_CAP]
+    HExc* xl = reinterpret_cast<HExc*>(xcnt + hx_count_words(G));                   // [NS][G][HX_CAP]
     uint64_t* full = reinterpret_cast<uint64_t*>(xl + NS * G * HX_CAP);             // [NS]
     uint64_t* empty = full + NS;                                                    // [NS]
 
