@@ -43,7 +43,7 @@ struct HExc {
 };
 
 // exception counts [NS][G] u32, padded to 16 bytes: the 8-byte lists and mbarriers follow
-constexpr int hx_count_words(int g) { return (H_NS * g + 3) & ~3; }
+__host__ __device__ constexpr int hx_count_words(int g) { return (H_NS * g + 3) & ~3; }
 
 size_t h16_smem_bytes(int g, uint32_t wmax) {
     return (size_t)H_NS * g * 4 * wmax                 // [NS][G][2 copies][wmax halves]
