@@ -607,7 +607,7 @@ __global__ void __launch_bounds__(32 * RMS_WARPS)
     };
 
     double a = 0.0, b = 0.0;
-    unsigned long long kept = 0;
+    uint32_t kept = 0;  // samples kept by one chain (< 2^32: series lengths are 32-bit)
     float cut = 0.0f;
     double rms0 = 0.0;
     for (int pass = 0; pass < 2; ++pass) {
@@ -629,18 +629,17 @@ __global__ void __launch_bounds__(32 * RMS_WARPS)
                 }
                 // double(v)*double(v) is exact (24+24 significant bits), so the
                 // reference's a += v*v (one rounding) is one DFMA, or an exact DMUL off
-                // the chain plus one DADD on it.  Pass 2 adds +0.0 for clipped samples:
-                // b is a sum of squares (never -0), so b + 0.0 == b and the chain is one
-                // DADD per sample instead of DFMA + select.
+                // the chain plus one DADD on it.  Pass 2 skips clipped samples with a
+                // predicated DADD: b is a sum of squares (never -0), so skipping equals the
+                // reference's adding nothing.
 #pragma unroll
                 for (int u = 0; u < RMS_U; ++u) {
                     const double dv = (double)v[u];
                     if (pass == 0) {
                         a = __fma_rn(dv, dv, a);
-                    } else {
-                        const bool keep = fabsf(v[u]) <= cut;
-                        b = __dadd_rn(b, keep ? __dmul_rn(dv, dv) : 0.0);
-                        kept += keep;
+                    } else if (fabsf(v[u]) <= cut) {  // b + 0.0 == b: skipping the add is the same
+                        b = __dadd_rn(b, __dmul_rn(dv, dv));
+                        ++kept;
                     }
                 }
             }
@@ -683,9 +682,9 @@ __global__ void __launch_bounds__(32 * RMS_WARPS)
             cut = __double2float_rn(__dmul_rn(3.0, rms0));
         } else {
             unsigned long long kt = kept;
-            kt += __shfl_down_sync(0xffffffffu, kept, 1, 4);
-            kt += __shfl_down_sync(0xffffffffu, kept, 2, 4);
-            kt += __shfl_down_sync(0xffffffffu, kept, 3, 4);
+            kt += (unsigned long long)__shfl_down_sync(0xffffffffu, kept, 1, 4);
+            kt += (unsigned long long)__shfl_down_sync(0xffffffffu, kept, 2, 4);
+            kt += (unsigned long long)__shfl_down_sync(0xffffffffu, kept, 3, 4);
             if (live && k == 0) {
                 uint8_t stt = 0;
                 double rms = rms0;
