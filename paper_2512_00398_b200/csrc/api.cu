@@ -1656,8 +1656,15 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                     PGB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
                     ctx->sub_events.push_back(e);
                 }
+                // the first piece ends where the first dedispersion tiles can run (every
+                // trial's delay plus two tiles); the rest of the chunk in equal pieces
+                int64_t maxd_all = 0;
+                for (uint32_t t = ctx->tr_begin; t < ctx->tr_end; ++t) maxd_all = std::max(maxd_all, ctx->maxd[t]);
+                const uint64_t first = std::min<uint64_t>(L0, round_up((uint64_t)maxd_all + 3 * DD_NT + 64, 64));
                 for (int j = 0; j < PGB_PROG_SUBSEG; ++j) {
-                    uint64_t e = j + 1 == PGB_PROG_SUBSEG ? L0 : round_up(L0 * (j + 1) / PGB_PROG_SUBSEG, 64);
+                    uint64_t e = j + 1 == PGB_PROG_SUBSEG
+                                     ? L0
+                                     : first + round_up((L0 - first) * j / (PGB_PROG_SUBSEG - 1), 64);
                     e = std::min(e, L0);
                     if (e > done) {
                         PGB_CUDA(cudaMemcpyAsync(ctx->payload.as<uint8_t>() + done * C, payload + done * C,
