@@ -112,6 +112,12 @@ struct pgb_context {
     cudaStream_t st = nullptr;
     cudaStream_t copy_st = nullptr;
     cudaStream_t rms_st = nullptr;  // robust RMS of chunk k overlaps the boxcar of chunk k-1
+    // asynchronous file-search back halves (boxcar, runs, append) run on bx_st, so their CTAs
+    // fill the SMs the persistent dedispersion of the next chunk leaves idle in its tail;
+    // ev_back[slot] marks a slot's back half done (the next front half of that slot waits)
+    cudaStream_t bx_st = nullptr;
+    cudaEvent_t ev_back[2] = {};
+    bool back_pending[2] = {false, false};
     cudaEvent_t ev_dd0[2] = {}, ev_dd1[2] = {}, ev_front[2] = {}, ev_rms[2] = {};
     // per-stage timing of the synchronous run_dm_loop path (TrialTiming, engine.hpp:16-23):
     // RMS start on rms_st, boxcar start / end and the end of the run order on the main stream
@@ -399,6 +405,10 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                  const pgb_engine_config* cfg, int slot, ChunkRun& run) {
     NvtxRange nvtx("pgb chunk front (transpose, dedispersion, baseline, rms)");
     cudaStream_t st = ctx->st;
+    if (ctx->back_pending[slot]) {  // the slot's buffers are still read by a back half on bx_st
+        PGB_CUDA(cudaStreamWaitEvent(st, ctx->ev_back[slot], 0));
+        ctx->back_pending[slot] = false;
+    }
     const uint64_t L = spec->length;
     const uint32_t C = ctx->nchans;
     run = ChunkRun{};
@@ -963,11 +973,12 @@ void chunk_back(pgb_context* ctx, ChunkRun& run) {
 // candidate sorts, candidates appended to ctx->file_cands at a device-side total, the
 // degenerate-trial flags copied to pinned host memory.  The file search reads all of it
 // once at the end and re-runs the file with larger capacities if a counter overflowed.
-void chunk_back_async(pgb_context* ctx, ChunkRun& run, uint8_t* h_status, uint64_t file_cap) {
+void chunk_back_async(pgb_context* ctx, ChunkRun& run, uint8_t* h_status, uint64_t file_cap,
+                      cudaStream_t st) {
     NvtxRange nvtx("pgb chunk back (async)");
-    cudaStream_t st = ctx->st;
     const int slot = run.slot;
     if (!run.live) return;
+    if (st != ctx->st) PGB_CUDA(cudaStreamWaitEvent(st, ctx->ev_front[slot], 0));  // dedispersion + baseline done
     const pgb_chunk_spec* spec = &run.spec;
     const pgb_engine_config* cfg = &run.cfg;
     PGB_CUDA(cudaStreamWaitEvent(st, ctx->ev_rms[slot], 0));
@@ -1284,7 +1295,9 @@ pgb_status pgb_create(int device, pgb_context** out) {
         PGB_CUDA(cudaStreamCreateWithFlags(&ctx->st, cudaStreamNonBlocking));
         PGB_CUDA(cudaStreamCreateWithFlags(&ctx->copy_st, cudaStreamNonBlocking));
         PGB_CUDA(cudaStreamCreateWithFlags(&ctx->rms_st, cudaStreamNonBlocking));
+        PGB_CUDA(cudaStreamCreateWithFlags(&ctx->bx_st, cudaStreamNonBlocking));
         for (int k = 0; k < 2; ++k) {
+            PGB_CUDA(cudaEventCreateWithFlags(&ctx->ev_back[k], cudaEventDisableTiming));
             PGB_CUDA(cudaEventCreate(&ctx->ev_dd0[k]));
             PGB_CUDA(cudaEventCreate(&ctx->ev_dd1[k]));
             PGB_CUDA(cudaEventCreate(&ctx->ev_front[k]));
@@ -1305,6 +1318,7 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         cudaStreamSynchronize(ctx->st);
         cudaStreamSynchronize(ctx->copy_st);
         cudaStreamSynchronize(ctx->rms_st);
+        cudaStreamSynchronize(ctx->bx_st);
         for (int k = 0; k < 2; ++k)
             for (DevBuf* b : {&ctx->base[k], &ctx->frms[k], &ctx->status[k], &ctx->d_row_len[k],
                               &ctx->slot_active[k]})
@@ -1319,7 +1333,9 @@ pgb_status pgb_destroy(pgb_context* ctx) {
                           &ctx->rfi.samp_bad, &ctx->rfi.dbl, &ctx->rfi.tmp, &ctx->rfi.rows, &ctx->cands_raw, &ctx->cands_sorted,
                           &ctx->frags, &ctx->frags_sorted, &ctx->counters, &ctx->sort_keys,
                           &ctx->sort_idx, &ctx->sort_tmp, &ctx->payload, &ctx->file_cands,
-                          &ctx->file_sorted, &ctx->cl_scratch, &ctx->clusters, &ctx->members, &ctx->d_levels, &ctx->d_wide})
+                          &ctx->file_sorted, &ctx->cl_scratch, &ctx->clusters, &ctx->members, &ctx->d_levels, &ctx->d_wide,
+                          &ctx->d_bxs, &ctx->ddf_win, &ctx->ddf_off, &ctx->ddh_win, &ctx->ddh_off, &ctx->rfi.xcnt,
+                          &ctx->rfi.xP, &ctx->rfi.xR, &ctx->rfi.xF})
             b->release();
         ctx->h_counters.release();
         for (auto e : ctx->seg_events) cudaEventDestroy(e);
@@ -1339,8 +1355,9 @@ pgb_status pgb_destroy(pgb_context* ctx) {
         for (int k = 0; k < 2; ++k)
             for (cudaEvent_t e : {ctx->ev_dd0[k], ctx->ev_dd1[k], ctx->ev_front[k], ctx->ev_rms[k], ctx->ev_rms0[k]})
                 cudaEventDestroy(e);
-        for (cudaEvent_t e : {ctx->ev_bx0, ctx->ev_bx1, ctx->ev_pk1}) cudaEventDestroy(e);
+        for (cudaEvent_t e : {ctx->ev_bx0, ctx->ev_bx1, ctx->ev_pk1, ctx->ev_back[0], ctx->ev_back[1]}) cudaEventDestroy(e);
         cudaStreamDestroy(ctx->rms_st);
+        cudaStreamDestroy(ctx->bx_st);
         cudaStreamDestroy(ctx->st);
         cudaStreamDestroy(ctx->copy_st);
         delete ctx;
@@ -1740,8 +1757,15 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
                     b.index = run.spec.index;
                     b.active = run.active;
                     b.skipped = run.skipped;
+                    // with a baseline the back half reads only its slot's buffers: it runs on
+                    // bx_st, beside the next chunk's dedispersion
+                    cudaStream_t bst = overlap && !pgb_ablation_env("PGB_BACK_MAIN") ? ctx->bx_st : ctx->st;
                     chunk_back_async(ctx, run, ctx->h_file_status.as<uint8_t>() + back_k * (size_t)max_rows,
-                                     file_cap);
+                                     file_cap, bst);
+                    if (bst != ctx->st && run.live) {
+                        PGB_CUDA(cudaEventRecord(ctx->ev_back[run.slot], bst));
+                        ctx->back_pending[run.slot] = true;
+                    }
                 }
                 ++back_k;
             };
@@ -1780,6 +1804,11 @@ pgb_status pgb_search_file_u8(pgb_context* ctx, const uint8_t* payload, int payl
         } else {
             for (;;) {
                 run_chunks();
+                for (int sl = 0; sl < 2; ++sl)  // the back halves on bx_st are done before the readback
+                    if (ctx->back_pending[sl]) {
+                        PGB_CUDA(cudaStreamWaitEvent(ctx->st, ctx->ev_back[sl], 0));
+                        ctx->back_pending[sl] = false;
+                    }
                 auto* hc = ctx->h_file_ctr.as<unsigned long long>();
                 PGB_CUDA(cudaMemcpyAsync(hc, ctx->file_ctr.p, 3 * sizeof(unsigned long long),
                                          cudaMemcpyDeviceToHost, ctx->st));
