@@ -1079,8 +1079,7 @@ __global__ void __launch_bounds__(BX_THREADS)
     if (lane == 0) s_amax[warp] = amax;
     // exact per-level cuts: cut_w = C 2^L with C the largest integer such that
     // fl(C 2^L sc_w) <= thr (monotone), so a multiple d of 2^L passes iff d > cut_w
-    uint32_t nlev = 0;
-    for (uint64_t w = 1; w <= bmax && w <= (uint64_t)n; w <<= 1) ++nlev;
+    const uint32_t nlev = 32 - __clz((uint32_t)min(bmax, (uint64_t)n));
     const double thr = ctx.cp.threshold;
     const double p2l = ldexp(1.0, max(L, -1074)), p2nl = ldexp(1.0, min(-L, 1023));
     if (warp == 0 && (uint32_t)lane < nlev) {
@@ -1146,13 +1145,14 @@ __global__ void __launch_bounds__(BX_THREADS)
         if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&s_mask, 1u << level);
     }
     __syncthreads();
-    const unsigned mask = s_mask;
-    // threshold runs of the flagged levels on contiguous strips, as the tree kernel
-    level = 0;
-    for (uint32_t w = 1; w <= (uint32_t)bmax && w <= n; w <<= 1, ++level) {
-        const uint32_t m = n - (uint32_t)w + 1;
+    // threshold runs of the flagged levels on contiguous strips, as the tree kernel (the
+    // mask's set bits only: most tiles flag none)
+    for (unsigned mask = s_mask; mask; mask &= mask - 1) {
+        level = __ffs(mask) - 1;
+        const uint32_t w = 1u << level;
+        const uint32_t m = n - w + 1;
         const uint32_t lim2 = m > i0 ? min(m - i0, T) : 0;
-        if (mask & (1u << level)) {
+        {
             const double sc = scale[level];
             const uint32_t lo = j0;
             const uint32_t hi = min(lo + S, lim2);
