@@ -26,7 +26,7 @@ import bench  # noqa: E402
 from tools import synth  # noqa: E402
 from paper_2512_00398_b200.engine import default_engine  # noqa: E402
 
-CONFIGS = {k: v for k, v in synth.CONFIGS.items() if k in ("A", "C", "E")}
+CONFIGS = {k: v for k, v in synth.CONFIGS.items() if k in ("A", "C", "E", "E1")}
 
 
 def run_file(cfg, steps, label=None):
@@ -125,6 +125,8 @@ def main():
             out = run_multi(args.steps, n_exec=args.n_exec)
         elif name == "Ddisk":
             out = run_multi_disk(args.steps, n_exec=args.n_exec)
+        elif name == "E1norfi":  # config E's geometry on the integer path (what RFI costs)
+            out = run_file(dict(synth.CONFIGS["E1"], rfi=False), args.steps, label="config_E_one_chunk_no_rfi")
         else:
             out = run_file(dict(CONFIGS[name]), args.steps)
         print(json.dumps(out), flush=True)
