@@ -69,11 +69,14 @@ def test_progressive_first_chunk_matches(monkeypatch):
         assert write_candidates(other.clusters) == write_candidates(a.clusters)
 
 
+@pytest.mark.parametrize("alt", ["PGB_SYNC_BACK", "PGB_BACK_MAIN"])
 @pytest.mark.parametrize("initial_cap", [None, "64"])
-def test_async_back_halves_match_sync(monkeypatch, initial_cap):
+def test_async_back_halves_match_sync(monkeypatch, initial_cap, alt):
     """The file search's back halves run without host round trips (device-side counts,
-    one read per file); the result must equal the per-chunk synchronous path
-    (PGB_SYNC_BACK=1), also when tiny initial buffers force the overflow-and-retry path."""
+    one read per file) on their own stream beside the next chunk's dedispersion; the result
+    must equal the per-chunk synchronous path (PGB_SYNC_BACK=1) and the back halves on the
+    main stream (PGB_BACK_MAIN=1), also when tiny initial buffers force the
+    overflow-and-retry path."""
     hdr = FilterbankHeader(fch1=1500.0, foff=-1.0, nchans=256, tsamp=64e-6, nsamples=3 << 15)
     params = SearchParams(dm_lo=0.0, dm_hi=300.0, spacing=LinearSpacing(2.0),
                           engine=EngineConfig(boxcar_max=1024), baseline_len_s=0.25,
@@ -86,8 +89,8 @@ def test_async_back_halves_match_sync(monkeypatch, initial_cap):
     res = []
     for sync in (False, True):
         if sync:
-            monkeypatch.setenv("PGB_SYNC_BACK", "1")
-        with Engine(0, ablations=sync) as eng:  # PGB_SYNC_BACK is an ablation switch
+            monkeypatch.setenv(alt, "1")
+        with Engine(0, ablations=sync) as eng:  # both are ablation switches
             res.append(eng.search_file(payload, hdr.nsamples, task.chunks, task.plan, task.engine))
     (a, ca, sa), (b, cb, sb) = res
     assert len(a) == len(b) > 0
