@@ -153,7 +153,8 @@ struct pgb_context {
     uint32_t dd_tab_wmax = 0;  // wmax the staging table was built for (0 = stale)
     DevBuf ddf_win, ddf_off;     // f32 staging table (non-integer float chunks)
     uint32_t ddf_tab_wmax = 0;
-    DevBuf ddh_win, ddh_off;     // fp16 staging table (RFI-masked 8-bit chunks with float rows)
+    DevBuf ddh_win, ddh_off;
+    DevBuf ddy_win, ddy_off, d_dirty;  // event-replay RFI kernel (ablation): tables, fallback flag     // fp16 staging table (RFI-masked 8-bit chunks with float rows)
     uint32_t ddh_tab_wmax = 0;
     std::vector<uint32_t> bad_rows_host;  // the current chunk's flagged rows (exception density)
     DevBuf file_cands, file_sorted;
@@ -279,6 +280,7 @@ struct ChunkInput {
     const uint8_t* chan_bad = nullptr;
     const uint8_t* samp_bad = nullptr;
     bool h16 = false;
+    bool hyb = false;  // (with u8) local-mean rows through the event-replay kernel (ablation)
     std::function<ChunkInput()> fallback;
     // progressive chunk whose pieces are uploaded by another thread (streaming search):
     // called with the piece index before its event is waited on; returns once the piece's
@@ -470,6 +472,8 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     for (uint32_t r = 0; r < nrows; ++r) blk_len[r / tb] = std::max(blk_len[r / tb], row_len[r]);
     const bool u8 = in.u8;
     const bool h16 = in.h16;  // RFI-masked 8-bit chunk with float rows: the fp16 in-order kernel
+    const bool hyb = in.hyb;  // ... or the event-replay kernel over the masked integer codes
+    const bool ints = u8 && !hyb;  // integer series (else fp32)
     if (u8 && C > PGB_MAX_EXACT_CHANS)
         raise(PGB_ERR_CONFIG, "8-bit input with more than 65793 channels: the integer channel sums pass "
                               "2^24, where the reference's fp32 sums start rounding (widen to floats)");
@@ -515,6 +519,28 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         }
     } else {
         while (g > 1 && dedisp_smem_bytes(u8, g, wmax) > DD_SMEM_BUDGET) g >>= 1;
+    }
+    if (hyb) {
+        // every block staged, integer sums below 2^21 (the merges' exactness bound), room for
+        // the head, at most HX_CAP flagged rows per staged window
+        const uint32_t hw = hyb_wmax(spread);
+        const std::vector<uint32_t>& R = ctx->bad_rows_host;
+        size_t dense = 0;
+        for (size_t lo = 0, hi = 0; hi < R.size(); ++hi) {
+            while ((uint64_t)R[hi] - R[lo] >= (uint64_t)hw + 4) ++lo;
+            dense = std::max(dense, hi - lo + 1);
+        }
+        const uint32_t cpad = (C + 7) & ~7u;
+        if (!wide_rows.empty() || !hyb_fits(hw) || (uint64_t)C * 255 >= (1u << 21) ||
+            cpad < hyb_head_channels() + 8 || dense > (size_t)HX_CAP) {
+            ChunkInput fb = in.fallback();
+            fb.more = in.more;
+            fb.ev0 = in.ev0;
+            fb.ev1 = in.ev1;
+            fb.pitch_min = in.pitch_min;
+            chunk_front(ctx, fb, spec, cfg, slot, run);
+            return;
+        }
     }
     // warp-specialized TMA kernel (u8): 16-byte aligned window starts, 256-byte boxes,
     // >= 20 bytes of slack for the packers' funnel shifts; deepest ring that fits
@@ -636,6 +662,40 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
         launch_dedisp_u8_ws(dw, ws_ns, ctx->rows.as<uint8_t>(), ctx->series.as<int32_t>(), st);
     } else
 #endif
+    if (hyb) {
+        dl.nchans_pad = C_pad;
+        dl.wmax = hyb_wmax(spread);
+        dl.ntiles = (uint32_t)((max_n + hyb_tile_len() - 1) / hyb_tile_len());
+        ctx->ddy_win.reserve((size_t)nblocks * C_pad * sizeof(uint2));
+        ctx->ddy_off.reserve((size_t)nblocks * C_pad * 32 * 4);
+        dl.dd_win = ctx->ddy_win.as<uint2>();
+        dl.dd_off = ctx->ddy_off.as<uint32_t>();
+        dl.xP = ctx->rfi.xP.as<uint32_t>();
+        dl.xR = ctx->rfi.xR.as<uint32_t>();
+        dl.xF = ctx->rfi.xF.as<float>();
+        dl.xlen = L;
+        ctx->d_work.reserve(64 * sizeof(uint32_t), true);
+        dl.work_ctr = ctx->d_work.as<uint32_t>();
+        ctx->d_dirty.reserve(sizeof(unsigned));
+        launch_dedisp_hyb(dl, ctx->rows.as<uint8_t>(), ctx->series.as<float>(), ctx->d_dirty.as<unsigned>(), st);
+        ctx->launches += 4;
+        ctx->h_counters.reserve(4 * sizeof(unsigned long long));
+        auto* hd = ctx->h_counters.as<unsigned long long>() + 3;
+        *hd = 0;
+        PGB_CUDA(cudaMemcpyAsync(hd, ctx->d_dirty.p, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+        PGB_CUDA(cudaStreamSynchronize(st));
+        static const bool which = getenv("PGB_DD_WHICH") != nullptr;
+        if (which && *hd) fprintf(stderr, "pgb rfi: event replay undecidable, chunk recomputed on the fp32 path\n");
+        if (*hd) {  // a state below 256 crossed two binades in one merge: the fp32 path
+            ChunkInput fb = in.fallback();
+            fb.more = in.more;
+            fb.ev0 = in.ev0;
+            fb.ev1 = in.ev1;
+            fb.pitch_min = in.pitch_min;
+            chunk_front(ctx, fb, spec, cfg, slot, run);
+            return;
+        }
+    } else
     if (u8) {
         dl.nchans_pad = C_pad;
         if (ctx->dd_tab_wmax != wmax) {
@@ -783,11 +843,11 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     // 3. baseline, 4. robust RMS (on rms_st: one sequential chain per thread, so it
     // leaves the SMs nearly idle and overlaps the previous chunk's boxcar)
     const void* work = ctx->series.p;
-    int kind = u8 ? 1 : 0;
+    int kind = ints ? 1 : 0;
     const uint32_t* d_len = ctx->d_row_len[slot].as<uint32_t>();
     if (baseline) {
         const uint64_t w = cfg->baseline_window % 2 == 0 ? cfg->baseline_window + 1 : cfg->baseline_window;
-        if (u8)
+        if (ints)
         {
             long long* bsums = nullptr;
             if (!pgb_ablation_env("PGB_BASELINE_SERIAL")) {
@@ -831,7 +891,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
     run.max_n = max_n;
     run.kind = kind;
     run.baseline = baseline;
-    run.u8 = u8;
+    run.u8 = ints;
     run.work = work;
 }
 
@@ -1139,6 +1199,21 @@ ChunkInput rfi_input(pgb_context* ctx, const uint8_t* cptr, uint64_t length, con
     ci.raw = false;  // the mask is chunk-local: no overlap reuse
     ci.chan_bad = ctx->rfi.chan_bad.as<uint8_t>();
     ci.samp_bad = ctx->rfi.samp_bad.as<uint8_t>();
+    if (nbs && rp.local_mean && pgb_ablation_env("PGB_RFI_HYB")) {
+        // the event-replay kernel over the masked integer codes (ablation library)
+        rfi_exceptions_u8(cptr, length, C, rp, ctx->rfi, nbs, ctx->st, &ctx->bad_rows_host);
+        ctx->launches += 4;
+        trace_mark(ctx, "rfi exceptions", ctx->st);
+        ci.hyb = true;
+        ci.fallback = [ctx, cptr, length, rp, nbc, nbs]() {
+            ctx->rfi_out.reserve((size_t)length * ctx->nchans * 4);
+            rfi_mask_impl<uint8_t>(cptr, length, ctx->nchans, rp, ctx->rfi, ctx->rfi_out.as<float>(), ctx->st,
+                                   nbc, nbs);
+            ctx->launches += 2;
+            return prepare_f32(ctx, ctx->rfi_out.as<float>(), length);
+        };
+        return ci;
+    }
     if (nbs && rp.local_mean && !pgb_ablation_env("PGB_RFI_H16")) {
         // local-mean rows: the widened float chunk and the in-order fp32 ring (the fp16
         // kernel with exception rows, PGB_RFI_H16=1 in the ablation library, measured

@@ -187,6 +187,14 @@ void launch_transpose_masked(const uint8_t* in, uint64_t length, uint32_t nchans
                              const uint8_t* samp_bad, void* rows, uint64_t pitch, bool h16, cudaStream_t st);
 // fp16 in-order kernel: staging table (p.wmax = halves per copy), launch, geometry
 constexpr int HX_CAP = 16;  // flagged rows per staged channel window (host-checked)
+// event-replay RFI kernel (dedisp_hyb.cu, ablation library): 512-output tiles, an in-order
+// fp32 head over the first hyb_head_channels() channels, `dirty` set when the chunk needs
+// the fp32 path instead
+uint32_t hyb_wmax(uint32_t spread);
+uint32_t hyb_tile_len();
+uint32_t hyb_head_channels();
+bool hyb_fits(uint32_t wmax);
+void launch_dedisp_hyb(const DedispLaunch& p, const uint8_t* rows, float* out, unsigned* dirty, cudaStream_t st);
 void launch_ddh_table(const DedispLaunch& p, uint2* win, uint32_t* off, cudaStream_t st);
 void launch_dedisp_h16(const DedispLaunch& p, const uint16_t* rows, float* out, cudaStream_t st);
 // widest stage that fits for a window of wmax halves per copy (0: none)

@@ -69,12 +69,14 @@ def _check(engine, ref, hdr, plan, data, rfi, *, eng=None):
     (30000, 512, 600.0, 3.0, 1000),
     (9000, 64, 40.0, 1.0, 250),
 ])
-@pytest.mark.parametrize("h16", [False, True])
-def test_local_mean_matches_reference(engine, abl_engine, ref, monkeypatch, L, nch, dm_hi, dm_step, every, h16):
+@pytest.mark.parametrize("kernel", [None, "PGB_RFI_H16", "PGB_RFI_HYB"])
+def test_local_mean_matches_reference(engine, abl_engine, ref, monkeypatch, L, nch, dm_hi, dm_step, every, kernel):
+    """Product (widened fp32 ring), the fp16 kernel and the event-replay kernel (ablation
+    library) against the reference's masked chunk through run_dm_loop."""
     hdr, plan, data = _case(L, nch, dm_hi, dm_step, every, seed=L + nch)
-    if h16:
-        monkeypatch.setenv("PGB_RFI_H16", "1")
-    bc, bs = _check(engine, ref, hdr, plan, data, RfiConfig(), eng=abl_engine if h16 else None)
+    if kernel:
+        monkeypatch.setenv(kernel, "1")
+    bc, bs = _check(engine, ref, hdr, plan, data, RfiConfig(), eng=abl_engine if kernel else None)
     assert bc.any() and bs.any()
 
 
