@@ -31,12 +31,9 @@ namespace pgb {
 namespace {
 
 constexpr int Y_NT = 512;            // outputs per tile
-constexpr int Y_WORDS = Y_NT / 128;  // 4-byte words per lane per trial
 constexpr int Y_NS = 3;              // ring slots
 constexpr int Y_G = 8;               // channels per stage
 constexpr int Y_TB = 32;             // trials per block
-constexpr int Y_TPW = 2;             // trials per warp
-constexpr int Y_Q = 4;               // events queued per lane before they are processed
 constexpr uint32_t Y_HEAD = 64;      // channels of the in-order fp32 head
 
 struct YExc {
@@ -54,6 +51,10 @@ size_t hyb_smem_bytes(uint32_t wmax) {
 }
 
 #ifdef PGB_ABLATIONS  // the kernels ship in the ablation library only
+constexpr int Y_WORDS = Y_NT / 128;  // 4-byte words per lane per trial
+constexpr int Y_TPW = 2;             // trials per warp
+constexpr int Y_Q = 4;               // events queued per lane before they are processed
+
 __device__ __forceinline__ uint32_t ymin(uint32_t v) {
     for (int o = 16; o; o >>= 1) v = min(v, __shfl_xor_sync(0xffffffffu, v, o));
     return v;
