@@ -760,6 +760,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                 if (in.seg_ready) in.seg_ready(segi);
                 ++segi;
                 PGB_CUDA(cudaStreamWaitEvent(st, seg.second, 0));
+                if (ctx->trace) trace_mark(ctx, "piece arrived", st);
                 if (b > a) {
                     launch_transpose_u8(static_cast<const uint8_t*>(in.data) + a * C, b - a, C,
                                         ctx->rows.as<uint8_t>() + a, rows_pitch, st);
@@ -776,6 +777,7 @@ void chunk_front(pgb_context* ctx, const ChunkInput& in, const pgb_chunk_spec* s
                     dd_launch(part);
                     ctx->launches += 1;
                     done = t_end;
+                    if (ctx->trace) trace_mark(ctx, "dedispersion piece", st);
                 }
             }
             if (done < ntiles) {  // (the last sub-segment ends at L, so this does not happen)
